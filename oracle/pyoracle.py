@@ -1,0 +1,209 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the CPU checkers.
+
+  liboracle.so                 plain-C restatement of the path (oracle/oracle.c)
+  _ref/libstencilcloth_ref.so  the UNMODIFIED reference sources compiled by oracle/Makefile,
+                               driven through oracle/ref_harness.cpp
+
+Importable only from tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs. Nothing in the product package imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+from paper_2403_12820_b200 import _abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libstencilcloth_ref.so")
+
+_P = C.c_void_p
+_I = C.c_int
+_CD = C.POINTER(_abi.sc_cloth_desc)
+_PR = C.POINTER(_abi.sc_params)
+
+
+def build(quiet: bool = True) -> None:
+    """make -C oracle (liboracle.so always; _ref only where /root/reference exists)."""
+    subprocess.run(["make", "-C", HERE], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Oracle:
+    """The C restatement, at float or double."""
+
+    def __init__(self):
+        if not os.path.exists(ORACLE_SO):
+            build()
+        self.lib = C.CDLL(ORACLE_SO)
+        for sfx, T in (("f32", C.c_float), ("f64", C.c_double)):
+            getattr(self.lib, "orc_forward_impulse_" + sfx).argtypes = [_I, _I, _PR, _P, _P, _P]
+            getattr(self.lib, "orc_plug_impulse_" + sfx).argtypes = [_I, _I, _CD, _P, _P, _P]
+            getattr(self.lib, "orc_advance_with_impulse_" + sfx).argtypes = [
+                _I, _I, _CD, _P, _P, _P, T, _P, _P, _P]
+            getattr(self.lib, "orc_nn_step_" + sfx).argtypes = [
+                _I, _I, _CD, _PR, _P, _P, T, _P, _P, _P, _P]
+            getattr(self.lib, "orc_rollout_" + sfx).argtypes = [
+                _I, _I, _I, _CD, _PR, _P, _P, _I, _I, _P]
+            for fn in ("orc_forward_impulse_", "orc_plug_impulse_", "orc_advance_with_impulse_",
+                       "orc_nn_step_", "orc_rollout_"):
+                getattr(self.lib, fn + sfx).restype = None
+
+    @staticmethod
+    def _dt(a):
+        return "f32" if a.dtype == np.float32 else "f64"
+
+    def forward_impulse(self, nx, ny, params, x, v):
+        out = np.empty_like(x)
+        getattr(self.lib, "orc_forward_impulse_" + self._dt(x))(nx, ny, C.byref(params), _p(x),
+                                                                _p(v), _p(out))
+        return out
+
+    def plug_impulse(self, nx, ny, cloth, x, v):
+        out = np.empty_like(x)
+        getattr(self.lib, "orc_plug_impulse_" + self._dt(x))(nx, ny, C.byref(cloth), _p(x), _p(v),
+                                                             _p(out))
+        return out
+
+    def advance_with_impulse(self, nx, ny, cloth, x, v, imp, t_next):
+        xo, vo = np.empty_like(x), np.empty_like(v)
+        m = np.zeros(nx * ny, np.uint8)
+        getattr(self.lib, "orc_advance_with_impulse_" + self._dt(x))(
+            nx, ny, C.byref(cloth), _p(x), _p(v), _p(imp), t_next, _p(xo), _p(vo), _p(m))
+        return xo, vo, m
+
+    def nn_step(self, nx, ny, cloth, params, x, v, t_next):
+        xo, vo, imp = np.empty_like(x), np.empty_like(v), np.empty_like(x)
+        m = np.zeros(nx * ny, np.uint8)
+        getattr(self.lib, "orc_nn_step_" + self._dt(x))(
+            nx, ny, C.byref(cloth), C.byref(params), _p(x), _p(v), t_next, _p(xo), _p(vo), _p(m),
+            _p(imp))
+        return xo, vo, m, imp
+
+    def rollout(self, nx, ny, cloths, params, x, v, steps, k0=0):
+        """run_steps<T> sequence over a batch; returns (x, v, last-step mask)."""
+        x, v = np.array(x, copy=True), np.array(v, copy=True)
+        batch = len(cloths)
+        arr = (_abi.sc_cloth_desc * batch)(*cloths)
+        m = np.zeros((batch, nx * ny), np.uint8)
+        getattr(self.lib, "orc_rollout_" + self._dt(x))(
+            nx, ny, batch, C.cast(arr, _CD), C.byref(params), _p(x), _p(v), steps, k0, _p(m))
+        return x, v, m
+
+
+class Reference:
+    """The reference's own code (oracle/_ref), through oracle/ref_harness.cpp."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path + " (build it with `make -C oracle ref` where "
+                                    "/root/reference exists)")
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_set_threads.argtypes = [_I]
+        L.ref_rollout_f32.argtypes = [_I, _I, _I, _CD, _PR, _P, _P, _I, _I, _P]
+        L.ref_rollout_tmpl_f64.argtypes = [_I, _I, _I, _CD, _PR, _P, _P, _I, _I, _P]
+        L.ref_step_f32.argtypes = [_I, _I, _CD, _PR, _P, _P, C.c_float, _P, _P, _P, _P]
+        L.ref_forward_impulse_f64.argtypes = [_I, _I, _PR, _P, _P, _P]
+        L.ref_plug_impulse_f64.argtypes = [_I, _I, _CD, _P, _P, _P]
+        L.ref_advance_with_impulse_f64.argtypes = [_I, _I, _CD, _P, _P, _P, C.c_double, _P, _P,
+                                                   _P]
+        L.ref_nn_step_f64.argtypes = [_I, _I, _CD, _PR, _P, _P, C.c_double, _P, _P]
+        L.ref_rollout_f64.argtypes = [_I, _I, _CD, _PR, _P, _P, _I, _P, _P]
+        L.ref_benchmark_net.argtypes = [_I, _I, _CD, _PR, _P, _P, _I, _I, _I, _I,
+                                        C.POINTER(C.c_double)]
+        L.ref_benchmark_net_cloth_parallel.argtypes = [_I, _I, _I, _CD, _PR, _P, _P, _I, _I,
+                                                       C.POINTER(C.c_double),
+                                                       C.POINTER(C.c_double)]
+
+    def _ck(self, rc):
+        if rc != 0:
+            msg = (self.lib.ref_last_error() or b"").decode()
+            if rc == 1:
+                raise ValueError(msg)
+            if rc == 2:
+                raise ArithmeticError(msg)
+            raise RuntimeError(msg)
+
+    def rollout_f32(self, nx, ny, cloths, params, x, v, steps, k0=0):
+        x = np.ascontiguousarray(x, np.float32).copy()
+        v = np.ascontiguousarray(v, np.float32).copy()
+        batch = len(cloths)
+        arr = (_abi.sc_cloth_desc * batch)(*cloths)
+        m = np.zeros((batch, nx * ny), np.uint8)
+        self._ck(self.lib.ref_rollout_f32(nx, ny, batch, C.cast(arr, _CD), C.byref(params), _p(x),
+                                          _p(v), steps, k0, _p(m)))
+        return x, v, m
+
+    def rollout_tmpl_f64(self, nx, ny, cloths, params, x, v, steps, k0=0):
+        x = np.ascontiguousarray(x, np.float64).copy()
+        v = np.ascontiguousarray(v, np.float64).copy()
+        batch = len(cloths)
+        arr = (_abi.sc_cloth_desc * batch)(*cloths)
+        m = np.zeros((batch, nx * ny), np.uint8)
+        self._ck(self.lib.ref_rollout_tmpl_f64(nx, ny, batch, C.cast(arr, _CD), C.byref(params),
+                                               _p(x), _p(v), steps, k0, _p(m)))
+        return x, v, m
+
+    def step_f32(self, nx, ny, cloth, params, x, v, t_next):
+        xo, vo, imp = (np.empty_like(x) for _ in range(3))
+        m = np.zeros(nx * ny, np.uint8)
+        self._ck(self.lib.ref_step_f32(nx, ny, C.byref(cloth), C.byref(params), _p(x), _p(v),
+                                       t_next, _p(xo), _p(vo), _p(m), _p(imp)))
+        return xo, vo, m, imp
+
+    def forward_impulse_f64(self, nx, ny, params, x, v):
+        out = np.empty_like(x)
+        self._ck(self.lib.ref_forward_impulse_f64(nx, ny, C.byref(params), _p(x), _p(v), _p(out)))
+        return out
+
+    def plug_impulse_f64(self, nx, ny, cloth, x, v):
+        out = np.empty_like(x)
+        self._ck(self.lib.ref_plug_impulse_f64(nx, ny, C.byref(cloth), _p(x), _p(v), _p(out)))
+        return out
+
+    def advance_with_impulse_f64(self, nx, ny, cloth, x, v, imp, t_next):
+        xo, vo = np.empty_like(x), np.empty_like(v)
+        m = np.zeros(nx * ny, np.uint8)
+        self._ck(self.lib.ref_advance_with_impulse_f64(nx, ny, C.byref(cloth), _p(x), _p(v),
+                                                       _p(imp), t_next, _p(xo), _p(vo), _p(m)))
+        return xo, vo, m
+
+    def nn_step_f64(self, nx, ny, cloth, params, x, v, t_next):
+        xo, vo = np.empty_like(x), np.empty_like(v)
+        self._ck(self.lib.ref_nn_step_f64(nx, ny, C.byref(cloth), C.byref(params), _p(x), _p(v),
+                                          t_next, _p(xo), _p(vo)))
+        return xo, vo
+
+    def rollout_f64(self, nx, ny, cloth, params, x0, v0, steps):
+        n = nx * ny
+        fx = np.empty((steps + 1, n, 3))
+        fv = np.empty_like(fx)
+        self._ck(self.lib.ref_rollout_f64(nx, ny, C.byref(cloth), C.byref(params), _p(x0), _p(v0),
+                                          steps, _p(fx), _p(fv)))
+        return fx, fv
+
+    def benchmark_net(self, nx, ny, cloth, params, x0, v0, steps, warmup, f64=False, threads=1):
+        sec = C.c_double()
+        self._ck(self.lib.ref_benchmark_net(nx, ny, C.byref(cloth), C.byref(params), _p(x0),
+                                            _p(v0), steps, warmup, int(f64), threads,
+                                            C.byref(sec)))
+        return sec.value
+
+    def benchmark_net_cloth_parallel(self, nx, ny, cloths, params, x0, v0, steps, warmup):
+        batch = len(cloths)
+        arr = (_abi.sc_cloth_desc * batch)(*cloths)
+        mx, wall = C.c_double(), C.c_double()
+        self._ck(self.lib.ref_benchmark_net_cloth_parallel(
+            nx, ny, batch, C.cast(arr, _CD), C.byref(params), _p(x0), _p(v0), steps, warmup,
+            C.byref(mx), C.byref(wall)))
+        return mx.value, wall.value

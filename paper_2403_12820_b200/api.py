@@ -1,0 +1,379 @@
+"""Reference-compatible compute API over the C-ABI (include/stencilcloth_b200.h).
+
+Drop-in functions for the reference's path (reference paths under /root/reference/proj):
+  forward_impulse(params, scene, positions, velocities)   bindings.cpp:147-154, net.cpp:132-142
+  plug_impulse(scene, positions, velocities)              sim.cpp:100-106
+  advance_with_impulse(scene, x, v, impulse, t_next)      sim.cpp:134-148
+  nn_step(params, scene, x, v, t_next)                    net.cpp:242-248
+  rollout(params, scene, steps=-1)                        bindings.cpp:163-164, eval.cpp:86-103
+  benchmark_net(params, scene, steps, warmup, precision)  eval.cpp:155-158
+They run the sm_100a kernels in PARITY mode at double precision by default, i.e. bit-identical
+to the reference's double-precision templates. `ClothBatch` is the batched, device-resident
+f32 engine the benchmarks drive (run_steps<float>, eval.cpp:35-67, over many cloths at once).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Union
+
+import numpy as np
+
+from . import _abi
+from .scene import (ConfigError, NetworkParams, NumericsError, Scene, Trajectory,
+                    STENCIL_OFFSETS)
+
+PRECISIONS = {"f32": _abi.SC_F32, "f64": _abi.SC_F64}
+MODES = {"parity": _abi.SC_MODE_PARITY, "fast": _abi.SC_MODE_FAST}
+
+
+class CudaError(RuntimeError):
+    """Device / driver failure (SC_ERR_CUDA). There is no CPU fallback."""
+
+
+def _raise(lib, code: int) -> None:
+    if code == _abi.SC_OK:
+        return
+    msg = (lib.sc_last_error() or b"").decode()
+    if code == _abi.SC_ERR_CONFIG:
+        raise ConfigError(msg)
+    if code == _abi.SC_ERR_NUMERICS:
+        raise NumericsError(msg)
+    if code == _abi.SC_ERR_CUDA:
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Context:
+    """One device context bound to a batch of same-size cloths and one parameter set."""
+
+    def __init__(self, scenes: Union[Scene, Sequence[Scene]], params: Optional[NetworkParams] = None,
+                 precision: str = "f64", device: int = 0, strip: Optional[tuple] = None):
+        self.lib = _abi.load()
+        scenes = [scenes] if isinstance(scenes, Scene) else list(scenes)
+        if not scenes:
+            raise ConfigError("batch: must be >= 1")
+        nx, ny = scenes[0].nx, scenes[0].ny
+        for s in scenes:
+            if (s.nx, s.ny) != (nx, ny):
+                raise ConfigError("batch: all cloths must share one grid size")
+        if precision not in PRECISIONS:
+            raise ConfigError("precision: must be 'f32' or 'f64'")
+        self.scenes, self.nx, self.ny, self.batch = scenes, nx, ny, len(scenes)
+        self.precision = precision
+        self.dtype = np.float32 if precision == "f32" else np.float64
+        h = C.c_void_p()
+        _raise(self.lib, self.lib.sc_ctx_create(device, PRECISIONS[precision], C.byref(h)))
+        self.h = h
+        self.strip = strip
+        if strip is not None:
+            _raise(self.lib, self.lib.sc_ctx_set_strip(self.h, int(strip[0]), int(strip[1])))
+        keep: list = []
+        descs = (_abi.sc_cloth_desc * self.batch)(*[s.cloth_desc(keep) for s in scenes])
+        sd = _abi.sc_scene_desc(nx, ny, self.batch, C.cast(descs, C.POINTER(_abi.sc_cloth_desc)))
+        _raise(self.lib, self.lib.sc_ctx_set_scene(self.h, C.byref(sd)))
+        if params is not None:
+            self.set_params(params)
+
+    # -- lifecycle --
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.sc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def local_rows(self) -> int:
+        if self.strip is None:
+            return self.ny
+        r0, n = self.strip
+        g0 = max(0, r0 - 2)
+        return min(self.ny, r0 + n + 2) - g0
+
+    def _arr(self, a, rows: Optional[int] = None) -> np.ndarray:
+        rows = self.local_rows if rows is None else rows
+        a = np.ascontiguousarray(a, dtype=self.dtype)
+        if a.size != self.batch * rows * self.nx * 3:
+            raise ConfigError("state shape does not match the grid topology")
+        return a
+
+    def _empty(self) -> np.ndarray:
+        return np.empty((self.batch, self.local_rows * self.nx, 3), dtype=self.dtype)
+
+    def set_params(self, params: NetworkParams) -> None:
+        c = params.to_c()
+        _raise(self.lib, self.lib.sc_ctx_set_params(self.h, C.byref(c)))
+
+    def set_state(self, x, v) -> None:
+        x, v = self._arr(x), self._arr(v)
+        _raise(self.lib, self.lib.sc_ctx_set_state(self.h, _ptr(x), _ptr(v)))
+
+    def get_state(self):
+        x, v = self._empty(), self._empty()
+        _raise(self.lib, self.lib.sc_ctx_get_state(self.h, _ptr(x), _ptr(v)))
+        return x, v
+
+    def advance(self, steps: int, k0: int = 0, mode: str = "parity") -> None:
+        _raise(self.lib, self.lib.sc_ctx_advance(self.h, int(steps), int(k0), MODES[mode]))
+
+    def sync(self) -> None:
+        _raise(self.lib, self.lib.sc_ctx_sync(self.h))
+
+    def health(self):
+        fi = np.zeros(self.batch, np.int32)
+        fn = np.zeros(self.batch, np.int32)
+        fs = np.zeros(self.batch, np.int32)
+        _raise(self.lib, self.lib.sc_ctx_get_health(self.h, _ptr(fi), _ptr(fn), _ptr(fs)))
+        return fi, fn, fs
+
+    def rollout(self, x0, v0, steps: int, k0: int = 0, mode: str = "parity",
+                constrained: bool = False):
+        x0, v0 = self._arr(x0), self._arr(v0)
+        xo, vo = self._empty(), self._empty()
+        m = np.zeros((self.batch, self.nx * self.ny), np.uint8) if constrained else None
+        _raise(self.lib, self.lib.sc_rollout(self.h, _ptr(x0), _ptr(v0), int(steps), int(k0),
+                                             MODES[mode], _ptr(xo), _ptr(vo), _ptr(m)))
+        return (xo, vo, m) if constrained else (xo, vo)
+
+    def rollout_frames(self, x0, v0, steps: int, stride: int = 1, mode: str = "parity"):
+        x0, v0 = self._arr(x0), self._arr(v0)
+        nf = steps // stride + 1
+        fx = np.empty((nf,) + (self.batch, self.local_rows * self.nx, 3), self.dtype)
+        fv = np.empty_like(fx)
+        _raise(self.lib, self.lib.sc_rollout_frames(self.h, _ptr(x0), _ptr(v0), int(steps),
+                                                    int(stride), MODES[mode], _ptr(fx), _ptr(fv)))
+        return fx, fv
+
+    def forward_impulse(self, x, v) -> np.ndarray:
+        x, v = self._arr(x), self._arr(v)
+        out = self._empty()
+        _raise(self.lib, self.lib.sc_forward_impulse(self.h, _ptr(x), _ptr(v), _ptr(out)))
+        return out
+
+    def plug_impulse(self, x, v) -> np.ndarray:
+        x, v = self._arr(x), self._arr(v)
+        out = self._empty()
+        _raise(self.lib, self.lib.sc_plug_impulse(self.h, _ptr(x), _ptr(v), _ptr(out)))
+        return out
+
+    def advance_with_impulse(self, x, v, impulse, t_next: float, constrained: bool = False):
+        x, v, imp = self._arr(x), self._arr(v), self._arr(impulse)
+        xo, vo = self._empty(), self._empty()
+        m = np.zeros((self.batch, self.nx * self.ny), np.uint8) if constrained else None
+        _raise(self.lib, self.lib.sc_advance_with_impulse(self.h, _ptr(x), _ptr(v), _ptr(imp),
+                                                          float(t_next), _ptr(xo), _ptr(vo),
+                                                          _ptr(m)))
+        return (xo, vo, m) if constrained else (xo, vo)
+
+    def nn_step(self, x, v, t_next: float, mode: str = "parity", constrained: bool = False):
+        x, v = self._arr(x), self._arr(v)
+        xo, vo = self._empty(), self._empty()
+        m = np.zeros((self.batch, self.nx * self.ny), np.uint8) if constrained else None
+        _raise(self.lib, self.lib.sc_nn_step(self.h, _ptr(x), _ptr(v), float(t_next),
+                                             MODES[mode], _ptr(xo), _ptr(vo), _ptr(m)))
+        return (xo, vo, m) if constrained else (xo, vo)
+
+    def benchmark(self, steps: int, warmup: int, mode: str = "parity") -> float:
+        sec = C.c_double()
+        _raise(self.lib, self.lib.sc_benchmark(self.h, int(steps), int(warmup), MODES[mode],
+                                               C.byref(sec)))
+        return sec.value
+
+    def launch_count(self) -> int:
+        return int(self.lib.sc_ctx_launch_count(self.h))
+
+    # -- strip decomposition helpers --
+    def halo_elems(self) -> int:
+        return int(self.lib.sc_ctx_halo_elems(self.h))
+
+    def halo_pack(self, side: int, dev_ptr: int, stream: Optional[int] = None) -> None:
+        _raise(self.lib, self.lib.sc_ctx_halo_pack(self.h, side, C.c_void_p(dev_ptr),
+                                                   C.c_void_p(stream) if stream else None))
+
+    def halo_unpack(self, side: int, dev_ptr: int, stream: Optional[int] = None) -> None:
+        _raise(self.lib, self.lib.sc_ctx_halo_unpack(self.h, side, C.c_void_p(dev_ptr),
+                                                     C.c_void_p(stream) if stream else None))
+
+    def strip_step(self, k: int, r_begin: int, r_end: int, mode: str = "fast",
+                   stream: Optional[int] = None) -> None:
+        _raise(self.lib, self.lib.sc_ctx_strip_step(self.h, int(k), int(r_begin), int(r_end),
+                                                    MODES[mode],
+                                                    C.c_void_p(stream) if stream else None))
+
+    def strip_commit(self) -> None:
+        _raise(self.lib, self.lib.sc_ctx_strip_commit(self.h))
+
+    def stream(self) -> int:
+        return int(self.lib.sc_ctx_stream(self.h) or 0)
+
+
+# ---------------------------------------------------------------- reference-style API ----
+
+def _state2(a, n: int, name: str) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] != 3:
+        raise ConfigError(name + ": expected an (n, 3) array")
+    return a
+
+
+def _check_shape(x, v, scene: Scene):
+    if x.shape[0] != v.shape[0]:
+        raise ConfigError("positions and velocities disagree on the node count")
+    if x.shape[0] != scene.node_count:
+        raise ConfigError("state shape does not match the grid topology")
+
+
+def _check_alpha(params: NetworkParams):
+    if not params.isru_alpha > 0.0:
+        raise ConfigError("isru_alpha: must be > 0")
+
+
+def _diagnose_forward(x, v, scene: Scene, p: NetworkParams, node: int) -> str:
+    """Names the branch with a non-finite value at one node, like diagnose_forward
+    (net.cpp:30-51). Failure path only: formats the error message."""
+    nx, ny = scene.nx, scene.ny
+    ix, iy = node % nx, node // nx
+    with np.errstate(all="ignore"):
+        lin = np.array(p.linear_b, dtype=np.float64)
+        non = np.zeros(3)
+        der = v[node] * p.self_velocity_w
+        for c, (dx, dy, _) in enumerate(STENCIL_OFFSETS):
+            jx, jy = ix + dx, iy + dy
+            if not (0 <= jx < nx and 0 <= jy < ny):
+                continue
+            j = jy * nx + jx
+            phi = (x[node] - x[j]) * p.kernel_gain[c]
+            xi = (v[node] - v[j]) * p.kernel_gain[c]
+            s = phi / np.sqrt(1.0 + p.isru_alpha * phi * phi)
+            lin = lin + phi * p.linear_w[c]
+            non = non + s * p.nonlinear_w[c]
+            der = der + xi * s * p.deriv_w[c]
+    branch = ("linear" if not np.all(np.isfinite(lin)) else
+              "nonlinear" if not np.all(np.isfinite(non)) else "derivative")
+    return "network impulse non-finite at node %d (%s branch)" % (node, branch)
+
+
+def forward_impulse(params: NetworkParams, scene: Scene, positions, velocities,
+                    device: int = 0) -> np.ndarray:
+    """Per-node impulse of the three-branch cell, float64 (net.cpp:132-142)."""
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    _check_alpha(params)
+    with Context(scene, params, "f64", device) as ctx:
+        out = ctx.forward_impulse(x, v)[0]
+        fi, fn, _ = ctx.health()
+    if fi[0] >= 0:
+        raise NumericsError(_diagnose_forward(x, v, scene, params, int(fn[0])))
+    return out
+
+
+def plug_impulse(scene: Scene, positions, velocities, device: int = 0) -> np.ndarray:
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    with Context(scene, None, "f64", device) as ctx:
+        return ctx.plug_impulse(x, v)[0]
+
+
+def advance_with_impulse(scene: Scene, positions, velocities, impulse, t_next: float,
+                         constrained: bool = False, device: int = 0):
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    imp = _state2(impulse, 0, "impulse")
+    _check_shape(x, v, scene)
+    if imp.shape != x.shape:
+        raise ConfigError("impulse field shape does not match the state")
+    with Context(scene, None, "f64", device) as ctx:
+        r = ctx.advance_with_impulse(x, v, imp, t_next, constrained)
+    if constrained:
+        return r[0][0], r[1][0], r[2][0]
+    return r[0][0], r[1][0]
+
+
+def nn_step(params: NetworkParams, scene: Scene, positions, velocities, t_next: float,
+            device: int = 0):
+    """One network step to the frame at t_next (net.cpp:242-248); returns (x, v)."""
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    _check_alpha(params)
+    with Context(scene, params, "f64", device) as ctx:
+        xo, vo = ctx.nn_step(x, v, t_next)
+        fi, fn, _ = ctx.health()
+    if fi[0] >= 0:
+        raise NumericsError(_diagnose_forward(x, v, scene, params, int(fn[0])))
+    return xo[0], vo[0]
+
+
+def apply_dirichlet(x: np.ndarray, v: np.ndarray, scene: Scene, t: float):
+    """Pins to the anchor path at time t (sim.cpp:108-117)."""
+    x, v = x.copy(), v.copy()
+    u = scene.bc.pin_velocity()
+    for k, i in enumerate(scene.bc.nodes):
+        x[i] = scene.bc.anchor_at(k, t)
+        v[i] = u
+    return x, v
+
+
+def rollout(params: NetworkParams, scene: Scene, steps: int = -1, device: int = 0) -> Trajectory:
+    """Closed-loop rollout storing every frame (eval.cpp:86-103), bit-identical to the
+    reference's double-precision rollout."""
+    scene.validate()
+    _check_alpha(params)
+    if steps < 0:
+        steps = scene.steps
+    x0, v0 = apply_dirichlet(scene.initial_x, scene.initial_v, scene, 0.0)
+    with Context(scene, params, "f64", device) as ctx:
+        fx, fv = ctx.rollout_frames(x0, v0, steps, 1, "parity")
+        fi, fn, fs = ctx.health()
+    bad_imp, bad_state = int(fi[0]), int(fs[0])
+    if bad_imp >= 0 and (bad_state < 0 or bad_imp <= bad_state):
+        k = bad_imp - 1
+        raise NumericsError(_diagnose_forward(fx[k, 0], fv[k, 0], scene, params, int(fn[0])))
+    if bad_state >= 0:
+        raise NumericsError("rollout diverged: non-finite state at frame %d" % bad_state)
+    return Trajectory(scene.nx, scene.ny, scene.dt, scene.spacing, fx[:, 0], fv[:, 0])
+
+
+@dataclass
+class BenchResult:
+    """eval.hpp:38-44."""
+    steps: int
+    warmup: int
+    precision: str
+    seconds: float
+    steps_per_second: float
+
+
+def benchmark_net(params: NetworkParams, scene: Scene, steps: int, warmup: int,
+                  precision: str = "f32", mode: str = "parity", device: int = 0) -> BenchResult:
+    """Device-timed run_steps loop (eval.cpp:69-82,155-158) from the scene's initial state."""
+    scene.validate()
+    if steps < 1:
+        raise ConfigError("bench: steps must be >= 1")
+    if warmup < 0:
+        raise ConfigError("bench: warmup must be >= 0")
+    with Context(scene, params, precision, device) as ctx:
+        ctx.set_state(scene.initial_x, scene.initial_v)
+        sec = ctx.benchmark(steps, warmup, mode)
+    return BenchResult(steps, warmup, precision, sec, steps / max(sec, 1e-12))
+
+
+class ClothBatch(Context):
+    """Batched device-resident engine: B same-size cloths stepped together (f32 by default)."""
+
+    def __init__(self, scenes: Sequence[Scene], params: NetworkParams, precision: str = "f32",
+                 device: int = 0, strip: Optional[tuple] = None):
+        super().__init__(scenes, params, precision, device, strip)

@@ -1,0 +1,923 @@
+// C-ABI implementation (include/stencilcloth_b200.h): contexts, validation, constant upload,
+// layout conversion at the edges, and launch of the PARITY / FAST step kernels.
+//
+// Error behaviour mirrors the reference: scene/param validation failures are SC_ERR_CONFIG with
+// the field name the reference's ConfigError would carry (scene.cpp:23-61, net.cpp:17-26);
+// there is no CPU fallback — a CUDA failure is SC_ERR_CUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stencilcloth_b200.h"
+#include "sc_device.cuh"
+#include "sc_kernels.h"
+
+using namespace scb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  sc_status code;
+  std::string msg;
+};
+
+[[noreturn]] void throw_config(const std::string& m) { throw Fail{SC_ERR_CONFIG, m}; }
+[[noreturn]] void throw_state(const std::string& m) { throw Fail{SC_ERR_STATE, m}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Fail{SC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <typename Fn>
+sc_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return SC_OK;
+  } catch (const Fail& f) {
+    g_err = f.msg;
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SC_ERR_STATE;
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encoder() {
+  static PFN_encodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_encodeTiled>(p);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+struct sc_ctx {
+  int device = 0;
+  sc_precision prec = SC_F32;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // grid / strip
+  int nx = 0, ny = 0, batch = 0;
+  int strip_row0 = -1, strip_rows = 0;  // requested strip (global rows), -1: whole cloth
+  int g0 = 0, rows_local = 0;           // global row of local row 0, local rows
+  int u0 = 0, u1 = 0;                   // owned global rows
+  int pitch = 0;
+  int64_t plane_stride = 0;
+  bool has_scene = false, has_params = false;
+  // device memory
+  void* state[2] = {nullptr, nullptr};
+  size_t state_bytes = 0;
+  int cur = 0;
+  void* cloths = nullptr;
+  void* spheres = nullptr;
+  void* planes = nullptr;
+  DevBuf<uint32_t> pin_bits;
+  DevBuf<int32_t> pin_rank;
+  void* anchors = nullptr;
+  DevBuf<Health> health;
+  DevBuf<uint8_t> mask;
+  DevBuf<unsigned char> aos;  // staging for AoS x, v, impulse
+  // params
+  NetConst<float> net32{};
+  NetConst<double> net64{};
+  FastNet fast{};
+  bool fast_ok = false;
+  FastPlan plan{};
+  CUtensorMap tmap[2];
+  bool tmap_ok = false;
+  std::atomic<int64_t> launches{0};
+
+  size_t elem() const { return prec == SC_F32 ? 4 : 8; }
+  int64_t nodes_global() const { return static_cast<int64_t>(nx) * ny; }
+  int64_t nodes_local() const { return static_cast<int64_t>(nx) * rows_local; }
+};
+
+namespace {
+
+void free_scene(sc_ctx* c) {
+  for (void*& p : c->state) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  for (void** p : {&c->cloths, &c->spheres, &c->planes, &c->anchors}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  c->pin_bits.release();
+  c->pin_rank.release();
+  c->health.release();
+  c->mask.release();
+  c->aos.release();
+  c->has_scene = false;
+  c->tmap_ok = false;
+}
+
+bool finite3(const double* v) {
+  return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]);
+}
+
+// Scene::validate (scene.cpp:23-61) + MaterialParams::validate (grid.cpp:73-81) for the fields
+// the NN step consumes; messages carry the reference's field names.
+void validate_scene(const sc_scene_desc* s) {
+  if (!s) throw_config("scene: null descriptor");
+  if (s->nx < 2) throw_config("grid.nx: must be >= 2");
+  if (s->ny < 2) throw_config("grid.ny: must be >= 2");
+  if (static_cast<int64_t>(s->nx) * s->ny > INT32_MAX)
+    throw_config("grid: node count exceeds the 32-bit node index of the reference");
+  if (s->batch < 1) throw_config("batch: must be >= 1");
+  if (!s->cloths) throw_config("batch: null cloth array");
+  const int64_t n = static_cast<int64_t>(s->nx) * s->ny;
+  for (int b = 0; b < s->batch; ++b) {
+    const sc_cloth_desc& c = s->cloths[b];
+    const std::string at = s->batch > 1 ? "cloths[" + std::to_string(b) + "]." : "";
+    if (!(c.mass > 0.0) || !std::isfinite(c.mass))
+      throw_config(at + "material.mass: must be a finite value > 0");
+    if (!std::isfinite(c.drag) || c.drag < 0.0)
+      throw_config(at + "material.drag: must be a finite value >= 0");
+    if (!std::isfinite(c.pressure)) throw_config(at + "material.pressure: must be finite");
+    if (!finite3(c.gravity)) throw_config(at + "material.gravity: components must be finite");
+    if (!(c.dt > 0.0) || !std::isfinite(c.dt))
+      throw_config(at + "time.dt: must be a finite value > 0");
+    if (c.n_pins < 0) throw_config(at + "pins: negative count");
+    if (c.n_pins > 0 && (!c.pin_nodes || !c.pin_anchors))
+      throw_config(at + "pins: anchor list does not match the node list");
+    for (int k = 0; k < c.n_pins; ++k) {
+      const int i = c.pin_nodes[k];
+      if (i < 0 || i >= n)
+        throw_config(at + "pins.nodes[" + std::to_string(k) + "]: index out of range");
+      if (k > 0 && c.pin_nodes[k - 1] >= i)
+        throw_config(at + "pins.nodes: must be strictly increasing (sorted, unique)");
+      if (!finite3(c.pin_anchors + 3 * k))
+        throw_config(at + "pins.anchors[" + std::to_string(k) + "]: non-finite component");
+    }
+    if (!finite3(c.pin_velocity))
+      throw_config(at + "pins.motion.velocity: components must be finite");
+    if (c.n_spheres < 0 || (c.n_spheres > 0 && !c.spheres))
+      throw_config(at + "colliders: bad sphere list");
+    for (int k = 0; k < c.n_spheres; ++k) {
+      const std::string path = at + "colliders[" + std::to_string(k) + "]";
+      const sc_sphere& sp = c.spheres[k];
+      if (!finite3(sp.center)) throw_config(path + ".center: components must be finite");
+      if (!(sp.radius > 0.0) || !std::isfinite(sp.radius))
+        throw_config(path + ".radius: must be a finite value > 0");
+      if (!(sp.friction >= 0.0 && sp.friction <= 1.0))
+        throw_config(path + ".friction: must be in [0, 1]");
+    }
+    if (c.n_planes < 0 || (c.n_planes > 0 && !c.planes))
+      throw_config(at + "planes: bad plane list");
+    for (int k = 0; k < c.n_planes; ++k) {
+      const std::string path = at + "planes[" + std::to_string(k) + "]";
+      if (!std::isfinite(c.planes[k].height)) throw_config(path + ".height: must be finite");
+      if (!(c.planes[k].friction >= 0.0 && c.planes[k].friction <= 1.0))
+        throw_config(path + ".friction: must be in [0, 1]");
+    }
+  }
+}
+
+template <typename T>
+T eps16() {
+  return std::numeric_limits<T>::epsilon() * T(16);
+}
+
+// SceneKernel<T> cast + the derived per-cloth products, each one IEEE op in T on the host
+// (x86-64 SSE, no contraction) exactly as the reference evaluates them (kernels.hpp:182-193,
+// 217, 221, 239).
+template <typename T>
+void upload_scene(sc_ctx* c, const sc_scene_desc* s) {
+  const int B = s->batch;
+  std::vector<ClothConst<T>> cl(static_cast<size_t>(B));
+  std::vector<SphereConst<T>> sph;
+  std::vector<PlaneConst<T>> pln;
+  std::vector<T> anchors;
+  const int64_t n = c->nodes_global();
+  const int64_t words = (n + 31) / 32;
+  int64_t total_words = 0;
+  for (int b = 0; b < B; ++b)
+    if (s->cloths[b].n_pins > 0) total_words += words;
+  std::vector<uint32_t> bits(static_cast<size_t>(std::max<int64_t>(total_words, 1)), 0u);
+  std::vector<int32_t> rank(bits.size(), 0);
+  int64_t word0 = 0;
+  for (int b = 0; b < B; ++b) {
+    const sc_cloth_desc& d = s->cloths[b];
+    ClothConst<T>& k = cl[static_cast<size_t>(b)];
+    k.dt = static_cast<T>(d.dt);
+    const T mass = static_cast<T>(d.mass);
+    k.scale = k.dt / mass;
+    k.drag_c = static_cast<T>(d.drag) * k.scale;
+    k.pressure = static_cast<T>(d.pressure);
+    for (int q = 0; q < 3; ++q) {
+      k.dv[q] = static_cast<T>(d.gravity[q]) * k.dt;
+      k.pin_u[q] = static_cast<T>(d.pin_velocity[q]);
+    }
+    k.plug_pressure = (d.plug_pressure && k.pressure != T(0)) ? 1 : 0;
+    k.plug_gravity = d.plug_gravity ? 1 : 0;
+    k.plug_drag = d.plug_drag ? 1 : 0;
+    k.n_spheres = d.n_spheres;
+    k.sphere0 = static_cast<int32_t>(sph.size());
+    for (int q = 0; q < d.n_spheres; ++q) {
+      SphereConst<T> sc{};
+      for (int e = 0; e < 3; ++e) sc.c[e] = static_cast<T>(d.spheres[q].center[e]);
+      sc.R = static_cast<T>(d.spheres[q].radius);
+      sc.Rband = sc.R * (T(1) + eps16<T>());
+      sc.omf = T(1) - static_cast<T>(d.spheres[q].friction);
+      sph.push_back(sc);
+    }
+    k.n_planes = d.n_planes;
+    k.plane0 = static_cast<int32_t>(pln.size());
+    for (int q = 0; q < d.n_planes; ++q) {
+      PlaneConst<T> pc{};
+      pc.h = static_cast<T>(d.planes[q].height);
+      const T ah = pc.h < T(0) ? -pc.h : pc.h;
+      pc.band = (ah > T(1) ? ah : T(1)) * eps16<T>();
+      pc.omf = T(1) - static_cast<T>(d.planes[q].friction);
+      pln.push_back(pc);
+    }
+    k.n_pins = d.n_pins;
+    k.pin_word0 = 0;
+    k.anchor0 = static_cast<int64_t>(anchors.size() / 3);
+    if (d.n_pins > 0) {
+      k.pin_word0 = word0;
+      for (int p = 0; p < d.n_pins; ++p) {
+        const int64_t node = d.pin_nodes[p];
+        bits[static_cast<size_t>(word0 + (node >> 5))] |= 1u << (node & 31);
+        for (int e = 0; e < 3; ++e) anchors.push_back(static_cast<T>(d.pin_anchors[3 * p + e]));
+      }
+      int32_t acc = 0;
+      for (int64_t w = 0; w < words; ++w) {
+        rank[static_cast<size_t>(word0 + w)] = acc;
+        acc += __builtin_popcount(bits[static_cast<size_t>(word0 + w)]);
+      }
+      word0 += words;
+    }
+  }
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    ck(cudaMalloc(dst, std::max<size_t>(bytes, 16)), "cudaMalloc(scene)");
+    if (bytes) ck(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy(scene)");
+  };
+  up(&c->cloths, cl.data(), sizeof(ClothConst<T>) * cl.size());
+  up(&c->spheres, sph.data(), sizeof(SphereConst<T>) * sph.size());
+  up(&c->planes, pln.data(), sizeof(PlaneConst<T>) * pln.size());
+  up(&c->anchors, anchors.data(), sizeof(T) * anchors.size());
+  c->pin_bits.ensure(bits.size());
+  ck(cudaMemcpy(c->pin_bits.p, bits.data(), sizeof(uint32_t) * bits.size(),
+                cudaMemcpyHostToDevice),
+     "cudaMemcpy(pins)");
+  c->pin_rank.ensure(rank.size());
+  ck(cudaMemcpy(c->pin_rank.p, rank.data(), sizeof(int32_t) * rank.size(),
+                cudaMemcpyHostToDevice),
+     "cudaMemcpy(pins)");
+}
+
+template <typename T>
+NetConst<T> make_net(const sc_params* p) {
+  NetConst<T> k{};
+  for (int c = 0; c < kChannels; ++c) {
+    k.gain[c] = static_cast<T>(p->kernel_gain[c]);
+    k.wl[c] = static_cast<T>(p->linear_w[c]);
+    k.wn[c] = static_cast<T>(p->nonlinear_w[c]);
+    k.wd[c] = static_cast<T>(p->deriv_w[c]);
+  }
+  for (int d = 0; d < 3; ++d) k.b[d] = static_cast<T>(p->linear_b[d]);
+  k.wv = static_cast<T>(p->self_velocity_w);
+  k.alpha = static_cast<T>(p->isru_alpha);
+  return k;
+}
+
+void build_tmaps(sc_ctx* c) {
+  c->tmap_ok = false;
+  if (c->prec != SC_F32) return;
+  PFN_encodeTiled enc = get_encoder();
+  if (!enc) throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver"};
+  for (int i = 0; i < 2; ++i) {
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->pitch),
+                                static_cast<cuuint64_t>(c->rows_local),
+                                static_cast<cuuint64_t>(6) * c->batch};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->pitch) * 4,
+                                   static_cast<cuuint64_t>(c->plane_stride) * 4};
+    const cuuint32_t box[3] = {136, 1, 6};  // see fast_kernels.cu (BOXW)
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(&c->tmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->state[i], dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+  }
+  c->tmap_ok = true;
+}
+
+void require_ready(sc_ctx* c, bool need_params = true) {
+  if (!c) throw_state("null context");
+  if (!c->has_scene) throw_state("no scene bound (call sc_ctx_set_scene first)");
+  if (need_params && !c->has_params) throw_state("no parameters bound (call sc_ctx_set_params)");
+}
+
+template <typename T>
+StepArgs<T> base_args(sc_ctx* c) {
+  StepArgs<T> a{};
+  a.in = static_cast<const T*>(c->state[c->cur]);
+  a.out = static_cast<T*>(c->state[1 - c->cur]);
+  a.plane_stride = c->plane_stride;
+  a.pitch = c->pitch;
+  a.nx = c->nx;
+  a.ny = c->ny;
+  a.g0 = c->g0;
+  a.u0 = c->u0;
+  a.u1 = c->u1;
+  a.batch = c->batch;
+  a.cloths = static_cast<const ClothConst<T>*>(c->cloths);
+  a.spheres = static_cast<const SphereConst<T>*>(c->spheres);
+  a.planes = static_cast<const PlaneConst<T>*>(c->planes);
+  a.pin_bits = c->pin_bits.p;
+  a.pin_rank = c->pin_rank.p;
+  a.pin_anchors = static_cast<const T*>(c->anchors);
+  return a;
+}
+
+template <typename T>
+NetConst<T>& net_of(sc_ctx* c);
+template <>
+NetConst<float>& net_of<float>(sc_ctx* c) {
+  return c->net32;
+}
+template <>
+NetConst<double>& net_of<double>(sc_ctx* c) {
+  return c->net64;
+}
+
+// One launch of the fused step (or one operator) on the ctx stream.
+template <typename T>
+void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, double t_next,
+                uint8_t* mask, T* impulse, Health* health, int u0, int u1, cudaStream_t stream) {
+  StepArgs<T> a = base_args<T>(c);
+  a.u0 = u0;
+  a.u1 = u1;
+  a.k = k;
+  a.use_t_override = t_override ? 1 : 0;
+  a.t_override = static_cast<T>(t_next);
+  a.constrained = mask;
+  a.impulse = impulse;
+  a.health = health;
+  a.net = net_of<T>(c);
+  cudaError_t e;
+  if constexpr (std::is_same<T, float>::value) {
+    if (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok) {
+      FastPlan plan = c->plan;
+      if (u0 != c->u0 || u1 != c->u1) plan = plan_fast(c->nx, u1 - u0, c->batch, c->device);
+      e = launch_fast(a, c->fast, &c->tmap[c->cur], plan, stream);
+    } else {
+      e = launch_parity<float>(a, kind, stream);
+    }
+  } else {
+    e = launch_parity<double>(a, kind, stream);
+  }
+  ck(e, "kernel launch");
+  c->launches.fetch_add(1);
+}
+
+void reset_health(sc_ctx* c) {
+  c->health.ensure(static_cast<size_t>(c->batch));
+  std::vector<Health> h(static_cast<size_t>(c->batch));
+  for (auto& x : h) {
+    x.impulse_key = ~0ull;
+    x.state_frame = INT_MAX;
+    x.pad = 0;
+  }
+  ck(cudaMemcpyAsync(c->health.p, h.data(), sizeof(Health) * h.size(), cudaMemcpyHostToDevice,
+                     c->stream),
+     "health reset");
+  ck(cudaStreamSynchronize(c->stream), "health reset");
+}
+
+void upload_state(sc_ctx* c, const void* x, const void* v) {
+  const size_t bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
+  c->aos.ensure(3 * bytes);
+  unsigned char* dx = c->aos.p;
+  unsigned char* dv = c->aos.p + bytes;
+  ck(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, c->stream), "H2D x");
+  ck(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, c->stream), "H2D v");
+  cudaError_t e;
+  if (c->prec == SC_F32)
+    e = launch_aos_to_planar<float>(reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
+                                    static_cast<float*>(c->state[c->cur]), c->batch, c->nx,
+                                    c->rows_local, c->plane_stride, c->pitch, c->stream);
+  else
+    e = launch_aos_to_planar<double>(reinterpret_cast<double*>(dx),
+                                     reinterpret_cast<double*>(dv),
+                                     static_cast<double*>(c->state[c->cur]), c->batch, c->nx,
+                                     c->rows_local, c->plane_stride, c->pitch, c->stream);
+  ck(e, "aos_to_planar");
+  c->launches.fetch_add(1);
+}
+
+void download_state(sc_ctx* c, int which, void* x, void* v, bool sync = true) {
+  const size_t bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
+  c->aos.ensure(3 * bytes);
+  unsigned char* dx = c->aos.p;
+  unsigned char* dv = c->aos.p + bytes;
+  cudaError_t e;
+  if (c->prec == SC_F32)
+    e = launch_planar_to_aos<float>(static_cast<const float*>(c->state[which]),
+                                    reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
+                                    c->batch, c->nx, c->rows_local, c->plane_stride, c->pitch,
+                                    c->stream);
+  else
+    e = launch_planar_to_aos<double>(static_cast<const double*>(c->state[which]),
+                                     reinterpret_cast<double*>(dx),
+                                     reinterpret_cast<double*>(dv), c->batch, c->nx,
+                                     c->rows_local, c->plane_stride, c->pitch, c->stream);
+  ck(e, "planar_to_aos");
+  c->launches.fetch_add(1);
+  if (x) ck(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H x");
+  if (v) ck(cudaMemcpyAsync(v, dv, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H v");
+  if (sync) ck(cudaStreamSynchronize(c->stream), "D2H sync");
+}
+
+void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last) {
+  if (steps < 0) throw_config("steps: must be >= 0");
+  if (mode != SC_MODE_PARITY && mode != SC_MODE_FAST) throw_config("mode: unknown");
+  if (mode == SC_MODE_FAST && c->prec != SC_F32)
+    throw_config("mode: FAST is an f32 mode (use PARITY with an f64 context)");
+  for (int s = 0; s < steps; ++s) {
+    const int k = k0 + s;
+    uint8_t* m = (s == steps - 1) ? dev_mask_last : nullptr;
+    if (c->prec == SC_F32)
+      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr, c->health.p, c->u0, c->u1,
+                        c->stream);
+    else
+      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr, c->health.p, c->u0,
+                         c->u1, c->stream);
+    c->cur = 1 - c->cur;
+  }
+}
+
+}  // namespace
+
+// ============================================================================ C ABI =====
+
+extern "C" {
+
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+
+const char* sc_last_error(void) { return g_err.c_str(); }
+
+sc_status sc_ctx_create(int device, sc_precision precision, sc_ctx** out) {
+  return guarded([&] {
+    if (!out) throw_config("out: null");
+    *out = nullptr;
+    if (precision != SC_F32 && precision != SC_F64) throw_config("precision: unknown");
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n)
+      throw Fail{SC_ERR_CUDA, "device " + std::to_string(device) + " not present (" +
+                                  std::to_string(n) + " visible)"};
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      throw Fail{SC_ERR_CUDA, std::string("kernels are built for sm_100a; device is ") +
+                                  prop.name};
+    auto* c = new sc_ctx();
+    c->device = device;
+    c->prec = precision;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreate(&c->ev0), "cudaEventCreate");
+    ck(cudaEventCreate(&c->ev1), "cudaEventCreate");
+    *out = c;
+  });
+}
+
+void sc_ctx_destroy(sc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_scene(c);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+sc_status sc_ctx_set_strip(sc_ctx* c, int32_t row0, int32_t rows) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    if (row0 < 0 || rows < 1) throw_config("strip: row0 must be >= 0 and rows >= 1");
+    c->strip_row0 = row0;
+    c->strip_rows = rows;
+  });
+}
+
+sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    validate_scene(s);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    free_scene(c);
+    c->nx = s->nx;
+    c->ny = s->ny;
+    c->batch = s->batch;
+    if (c->strip_row0 >= 0) {
+      if (s->batch != 1) throw_config("strip: row-strip decomposition needs batch == 1");
+      if (c->strip_row0 + c->strip_rows > s->ny) throw_config("strip: rows exceed grid.ny");
+      c->u0 = c->strip_row0;
+      c->u1 = c->strip_row0 + c->strip_rows;
+      c->g0 = std::max(0, c->u0 - 2);
+      c->rows_local = std::min(s->ny, c->u1 + 2) - c->g0;
+    } else {
+      c->u0 = 0;
+      c->u1 = s->ny;
+      c->g0 = 0;
+      c->rows_local = s->ny;
+    }
+    c->pitch = (s->nx + 3) / 4 * 4;
+    c->plane_stride = static_cast<int64_t>(c->rows_local) * c->pitch;
+    c->state_bytes = static_cast<size_t>(c->batch) * 6 * c->plane_stride * c->elem();
+    for (int i = 0; i < 2; ++i) {
+      ck(cudaMalloc(&c->state[i], c->state_bytes), "cudaMalloc(state)");
+      ck(cudaMemsetAsync(c->state[i], 0, c->state_bytes, c->stream), "memset(state)");
+    }
+    c->cur = 0;
+    if (c->prec == SC_F32)
+      upload_scene<float>(c, s);
+    else
+      upload_scene<double>(c, s);
+    c->health.ensure(static_cast<size_t>(c->batch));
+    reset_health(c);
+    if (c->prec == SC_F32) {
+      build_tmaps(c);
+      c->plan = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device);
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->has_scene = true;
+  });
+}
+
+sc_status sc_ctx_set_params(sc_ctx* c, const sc_params* p) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    if (!p) throw_config("params: null");
+    if (!(p->isru_alpha > 0.0)) throw_config("isru_alpha: must be > 0");
+    c->net32 = make_net<float>(p);
+    c->net64 = make_net<double>(p);
+    c->fast = make_fast_net(c->net32);
+    c->fast_ok = fast_supported(c->net32);
+    c->has_params = true;
+  });
+}
+
+sc_status sc_ctx_set_state(sc_ctx* c, const void* x, const void* v) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (!x || !v) throw_config("state: null array");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    upload_state(c, x, v);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+sc_status sc_ctx_get_state(sc_ctx* c, void* x, void* v) {
+  return guarded([&] {
+    require_ready(c, false);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    download_state(c, c->cur, x, v);
+  });
+}
+
+sc_status sc_ctx_advance(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mode) {
+  return guarded([&] {
+    require_ready(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    advance_impl(c, steps, k0, mode, nullptr);
+  });
+}
+
+sc_status sc_ctx_sync(sc_ctx* c) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+sc_status sc_ctx_get_health(sc_ctx* c, int32_t* bad_imp_frame, int32_t* bad_imp_node,
+                            int32_t* bad_state_frame) {
+  return guarded([&] {
+    require_ready(c, false);
+    std::vector<Health> h(static_cast<size_t>(c->batch));
+    ck(cudaMemcpyAsync(h.data(), c->health.p, sizeof(Health) * h.size(), cudaMemcpyDeviceToHost,
+                       c->stream),
+       "D2H health");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    for (int b = 0; b < c->batch; ++b) {
+      const Health& x = h[static_cast<size_t>(b)];
+      const bool imp_bad = x.impulse_key != ~0ull;
+      if (bad_imp_frame) bad_imp_frame[b] = imp_bad ? static_cast<int32_t>(x.impulse_key >> 32) : -1;
+      if (bad_imp_node)
+        bad_imp_node[b] = imp_bad ? static_cast<int32_t>(x.impulse_key & 0xffffffffu) : -1;
+      if (bad_state_frame) bad_state_frame[b] = x.state_frame == INT_MAX ? -1 : x.state_frame;
+    }
+  });
+}
+
+sc_status sc_rollout(sc_ctx* c, const void* x0, const void* v0, int32_t steps, int32_t k0,
+                     sc_mode mode, void* x_out, void* v_out, uint8_t* constrained) {
+  return guarded([&] {
+    require_ready(c);
+    if (!x0 || !v0) throw_config("state: null array");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_health(c);
+    upload_state(c, x0, v0);
+    uint8_t* dm = nullptr;
+    if (constrained && steps > 0) {
+      c->mask.ensure(static_cast<size_t>(c->batch) * c->nodes_global());
+      dm = c->mask.p;
+    }
+    advance_impl(c, steps, k0, mode, dm);
+    download_state(c, c->cur, x_out, v_out, false);
+    if (constrained) {
+      const size_t n = static_cast<size_t>(c->batch) * c->nodes_global();
+      if (dm)
+        ck(cudaMemcpyAsync(constrained, dm, n, cudaMemcpyDeviceToHost, c->stream), "D2H mask");
+      else
+        std::memset(constrained, 0, n);
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+sc_status sc_rollout_frames(sc_ctx* c, const void* x0, const void* v0, int32_t steps,
+                            int32_t stride, sc_mode mode, void* fx, void* fv) {
+  return guarded([&] {
+    require_ready(c);
+    if (stride < 1) throw_config("stride: must be >= 1");
+    if (!x0 || !v0 || !fx || !fv) throw_config("frames: null array");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_health(c);
+    upload_state(c, x0, v0);
+    const size_t frame_bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
+    std::memcpy(fx, x0, frame_bytes);
+    std::memcpy(fv, v0, frame_bytes);
+    int f = 1;
+    for (int k = 0; k < steps; k += stride) {
+      const int n = std::min(stride, steps - k);
+      advance_impl(c, n, k, mode, nullptr);
+      if (n == stride) {
+        download_state(c, c->cur, static_cast<unsigned char*>(fx) + frame_bytes * f,
+                       static_cast<unsigned char*>(fv) + frame_bytes * f);
+        ++f;
+      }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// Shared body of the per-operator entry points: the state is uploaded into the ctx front
+// buffer (these calls replace the resident state), the impulse staged as AoS.
+template <typename T>
+void op_call(sc_ctx* c, int kind, sc_mode mode, const void* x, const void* v,
+             const void* impulse_in, void* impulse_out, double t_next, void* xo, void* vo,
+             uint8_t* constrained) {
+  const size_t bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * sizeof(T);
+  upload_state(c, x, v);
+  T* dimp = reinterpret_cast<T*>(c->aos.p + 2 * bytes);
+  if (impulse_in)
+    ck(cudaMemcpyAsync(dimp, impulse_in, bytes, cudaMemcpyHostToDevice, c->stream), "H2D imp");
+  uint8_t* dm = nullptr;
+  if (constrained) {
+    c->mask.ensure(static_cast<size_t>(c->batch) * c->nodes_global());
+    dm = c->mask.p;
+  }
+  launch_one<T>(c, kind, mode, 0, true, t_next, dm, dimp, c->health.p, c->u0, c->u1, c->stream);
+  if (impulse_out)
+    ck(cudaMemcpyAsync(impulse_out, dimp, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H imp");
+  if (kind == KIND_STEP || kind == KIND_ADVANCE) {
+    download_state(c, 1 - c->cur, xo, vo, false);
+    if (constrained)
+      ck(cudaMemcpyAsync(constrained, dm, static_cast<size_t>(c->batch) * c->nodes_global(),
+                         cudaMemcpyDeviceToHost, c->stream),
+         "D2H mask");
+  }
+  ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+sc_status op_entry(sc_ctx* c, int kind, sc_mode mode, const void* x, const void* v,
+                   const void* imp_in, void* imp_out, double t_next, void* xo, void* vo,
+                   uint8_t* constrained, bool need_params) {
+  return guarded([&] {
+    require_ready(c, need_params);
+    if (!x || !v) throw_config("state: null array");
+    if (c->strip_row0 >= 0) throw_config("per-operator entry points need a whole-cloth context");
+    if (mode == SC_MODE_FAST && c->prec != SC_F32) throw_config("mode: FAST is an f32 mode");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    reset_health(c);
+    if (c->prec == SC_F32)
+      op_call<float>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
+    else
+      op_call<double>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
+  });
+}
+}  // namespace
+
+extern "C" {
+
+sc_status sc_forward_impulse(sc_ctx* c, const void* x, const void* v, void* impulse) {
+  if (!impulse) {
+    g_err = "impulse: null array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_FORWARD, SC_MODE_PARITY, x, v, nullptr, impulse, 0.0, nullptr, nullptr,
+                  nullptr, true);
+}
+
+sc_status sc_plug_impulse(sc_ctx* c, const void* x, const void* v, void* impulse) {
+  if (!impulse) {
+    g_err = "impulse: null array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_PLUG, SC_MODE_PARITY, x, v, nullptr, impulse, 0.0, nullptr, nullptr,
+                  nullptr, false);
+}
+
+sc_status sc_advance_with_impulse(sc_ctx* c, const void* x, const void* v, const void* impulse,
+                                  double t_next, void* xo, void* vo, uint8_t* constrained) {
+  if (!impulse || !xo || !vo) {
+    g_err = "advance_with_impulse: null array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_ADVANCE, SC_MODE_PARITY, x, v, impulse, nullptr, t_next, xo, vo,
+                  constrained, false);
+}
+
+sc_status sc_nn_step(sc_ctx* c, const void* x, const void* v, double t_next, sc_mode mode,
+                     void* xo, void* vo, uint8_t* constrained) {
+  if (!xo || !vo) {
+    g_err = "nn_step: null output array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_STEP, mode, x, v, nullptr, nullptr, t_next, xo, vo, constrained, true);
+}
+
+sc_status sc_benchmark(sc_ctx* c, int32_t steps, int32_t warmup, sc_mode mode, double* seconds) {
+  return guarded([&] {
+    require_ready(c);
+    if (steps < 1) throw_config("bench: steps must be >= 1");
+    if (warmup < 0) throw_config("bench: warmup must be >= 0");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    advance_impl(c, warmup, 0, mode, nullptr);
+    ck(cudaEventRecord(c->ev0, c->stream), "event");
+    advance_impl(c, steps, warmup, mode, nullptr);
+    ck(cudaEventRecord(c->ev1, c->stream), "event");
+    ck(cudaEventSynchronize(c->ev1), "event sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
+    if (seconds) *seconds = ms * 1e-3;
+  });
+}
+
+int64_t sc_ctx_halo_elems(sc_ctx* c) { return c ? static_cast<int64_t>(6) * 2 * c->nx : 0; }
+
+}  // extern "C"
+
+namespace {
+void halo_copy(sc_ctx* c, int side, void* dev, bool pack, cudaStream_t st) {
+  require_ready(c, false);
+  if (c->strip_row0 < 0) throw_config("halo: context has no strip");
+  if (side != 0 && side != 1) throw_config("halo: side must be 0 or 1");
+  // pack: owned rows next to the edge; unpack: ghost rows beyond the edge
+  int grow;
+  if (pack)
+    grow = side == 0 ? c->u0 : c->u1 - 2;
+  else
+    grow = side == 0 ? c->u0 - 2 : c->u1;
+  const size_t e = c->elem();
+  unsigned char* buf = static_cast<unsigned char*>(c->state[1 - c->cur]);
+  for (int r = 0; r < 2; ++r) {
+    const int g = grow + r;
+    if (g < 0 || g >= c->ny) continue;
+    const int lr = g - c->g0;
+    for (int p = 0; p < 6; ++p) {
+      unsigned char* dst_state = buf + (static_cast<size_t>(p) * c->plane_stride +
+                                        static_cast<size_t>(lr) * c->pitch) * e;
+      unsigned char* hal = static_cast<unsigned char*>(dev) +
+                           (static_cast<size_t>(p) * 2 + r) * c->nx * e;
+      if (pack)
+        ck(cudaMemcpyAsync(hal, dst_state, c->nx * e, cudaMemcpyDeviceToDevice, st), "halo");
+      else
+        ck(cudaMemcpyAsync(dst_state, hal, c->nx * e, cudaMemcpyDeviceToDevice, st), "halo");
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+sc_status sc_ctx_halo_pack(sc_ctx* c, int32_t side, void* dev_dst, void* stream) {
+  return guarded([&] {
+    halo_copy(c, side, dev_dst, true, stream ? static_cast<cudaStream_t>(stream) : c->stream);
+  });
+}
+
+sc_status sc_ctx_halo_unpack(sc_ctx* c, int32_t side, const void* dev_src, void* stream) {
+  return guarded([&] {
+    halo_copy(c, side, const_cast<void*>(dev_src), false,
+              stream ? static_cast<cudaStream_t>(stream) : c->stream);
+  });
+}
+
+sc_status sc_ctx_strip_step(sc_ctx* c, int32_t k, int32_t r_begin, int32_t r_end, sc_mode mode,
+                            void* stream) {
+  return guarded([&] {
+    require_ready(c);
+    if (r_begin < c->u0 || r_end > c->u1 || r_begin > r_end)
+      throw_config("strip_step: rows outside the owned strip");
+    if (mode == SC_MODE_FAST && c->prec != SC_F32) throw_config("mode: FAST is an f32 mode");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    if (c->prec == SC_F32)
+      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, c->health.p, r_begin,
+                        r_end, st);
+    else
+      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, c->health.p,
+                         r_begin, r_end, st);
+  });
+}
+
+sc_status sc_ctx_strip_commit(sc_ctx* c) {
+  return guarded([&] {
+    require_ready(c, false);
+    c->cur = 1 - c->cur;
+  });
+}
+
+void* sc_ctx_stream(sc_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+sc_status sc_ctx_state_buffers(sc_ctx* c, void** front, void** back, int64_t* plane_stride,
+                               int32_t* pitch, int32_t* local_rows, int32_t* row_base) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (front) *front = c->state[c->cur];
+    if (back) *back = c->state[1 - c->cur];
+    if (plane_stride) *plane_stride = c->plane_stride;
+    if (pitch) *pitch = c->pitch;
+    if (local_rows) *local_rows = c->rows_local;
+    if (row_base) *row_base = c->g0;
+  });
+}
+
+sc_status sc_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) throw_config("out: null");
+    ck(cudaHostAlloc(out, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+  });
+}
+
+void sc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int64_t sc_ctx_launch_count(sc_ctx* c) { return c ? c->launches.load() : 0; }
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Layout conversion at the C-ABI edge: the reference's AoS VecT<T>[node] (vec3.hpp:9-59)
+// <-> the planar SoA device layout of the step kernels (sc_device.cuh). Only the API edges
+// run these; device-resident stepping never converts.
+#include "sc_kernels.h"
+
+namespace scb {
+namespace {
+
+template <typename T>
+__global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, T* __restrict__ out,
+                              int batch, int nx, int rows, int64_t plane_stride, int pitch) {
+  const int64_t per = static_cast<int64_t>(rows) * nx;
+  const int64_t total = per * batch;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / per;
+    const int64_t node = i - b * per;
+    const int64_t r = node / nx;
+    const int64_t c = node - r * nx;
+    T* o = out + b * 6 * plane_stride + r * pitch + c;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      o[d * plane_stride] = x[3 * i + d];
+      o[(3 + d) * plane_stride] = v[3 * i + d];
+    }
+  }
+}
+
+template <typename T>
+__global__ void planar_to_aos(const T* __restrict__ in, T* __restrict__ x, T* __restrict__ v,
+                              int batch, int nx, int rows, int64_t plane_stride, int pitch) {
+  const int64_t per = static_cast<int64_t>(rows) * nx;
+  const int64_t total = per * batch;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / per;
+    const int64_t node = i - b * per;
+    const int64_t r = node / nx;
+    const int64_t c = node - r * nx;
+    const T* s = in + b * 6 * plane_stride + r * pitch + c;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (x) x[3 * i + d] = s[d * plane_stride];
+      if (v) v[3 * i + d] = s[(3 + d) * plane_stride];
+    }
+  }
+}
+
+int grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 64) g = 148 * 64;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_aos_to_planar(const T* x, const T* v, T* planar, int batch, int nx, int rows,
+                                 int64_t plane_stride, int pitch, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(batch) * rows * nx;
+  aos_to_planar<T><<<grid_for(total), 256, 0, stream>>>(x, v, planar, batch, nx, rows,
+                                                       plane_stride, pitch);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_planar_to_aos(const T* planar, T* x, T* v, int batch, int nx, int rows,
+                                 int64_t plane_stride, int pitch, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(batch) * rows * nx;
+  planar_to_aos<T><<<grid_for(total), 256, 0, stream>>>(planar, x, v, batch, nx, rows,
+                                                       plane_stride, pitch);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_aos_to_planar<float>(const float*, const float*, float*, int, int, int,
+                                                 int64_t, int, cudaStream_t);
+template cudaError_t launch_aos_to_planar<double>(const double*, const double*, double*, int, int,
+                                                  int, int64_t, int, cudaStream_t);
+template cudaError_t launch_planar_to_aos<float>(const float*, float*, float*, int, int, int,
+                                                 int64_t, int, cudaStream_t);
+template cudaError_t launch_planar_to_aos<double>(const double*, double*, double*, int, int, int,
+                                                  int64_t, int, cudaStream_t);
+
+}  // namespace scb

@@ -1,0 +1,267 @@
+// Device-side definitions shared by the PARITY and FAST step kernels.
+//
+// HBM layout: one ctx holds `batch` cloths; cloth b's state is 6 planar fields
+//   plane p in {x.x, x.y, x.z, v.x, v.y, v.z}, row r (local), column c:
+//   state[(b*6 + p) * plane_stride + r * pitch + c],   plane_stride = rows_local * pitch
+// with pitch = nx rounded up to 4 (16-byte rows for float4/TMA). Validity masks, pins and
+// collider constants are computed from (ix, iy) or read from small per-cloth tables, so a step
+// moves exactly 48 B per node (f32): x and v read once and written once.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace scb {
+
+constexpr int kChannels = 12;
+
+// canonical channel order E,N,W,S,NE,NW,SW,SE,E2,N2,W2,S2 (reference grid.cpp:14-30)
+__host__ __device__ constexpr int off_dx(int c) {
+  return c == 0 ? 1 : c == 1 ? 0 : c == 2 ? -1 : c == 3 ? 0 : c == 4 ? 1 : c == 5 ? -1
+       : c == 6 ? -1 : c == 7 ? 1 : c == 8 ? 2 : c == 9 ? 0 : c == 10 ? -2 : 0;
+}
+__host__ __device__ constexpr int off_dy(int c) {
+  return c == 0 ? 0 : c == 1 ? 1 : c == 2 ? 0 : c == 3 ? -1 : c == 4 ? 1 : c == 5 ? 1
+       : c == 6 ? -1 : c == 7 ? -1 : c == 8 ? 0 : c == 9 ? 2 : c == 10 ? 0 : -2;
+}
+
+// IEEE round-to-nearest primitives that can never be contracted into FMA. The parity kernels
+// and the shared plug/advance stage use only these, so they reproduce the reference's x86
+// SSE scalar arithmetic bit for bit.
+template <typename T>
+struct RN;
+template <>
+struct RN<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+  static __device__ __forceinline__ bool finite(float a) { return isfinite(a); }
+};
+template <>
+struct RN<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+  static __device__ __forceinline__ bool finite(double a) { return isfinite(a); }
+};
+
+// NetKernel<T> (reference kernels.hpp:255-260), cast once on the host (net_kernel.hpp:8-22).
+template <typename T>
+struct NetConst {
+  T gain[kChannels], wl[kChannels], wn[kChannels], wd[kChannels];
+  T b[3];
+  T wv, alpha;
+};
+
+// Per-cloth SceneKernel<T> constants (kernels.hpp:41-56) with the derived products the
+// reference computes in T inside add_plug_impulse / advance_with_impulse precomputed on the
+// host with the same single IEEE operation (so they are bit-identical).
+template <typename T>
+struct ClothConst {
+  T dt;
+  T scale;     // dt / mass                          (kernels.hpp:182)
+  T drag_c;    // drag * scale                       (kernels.hpp:193)
+  T pressure;  //                                    (kernels.hpp:183)
+  T dv[3];     // gravity * dt                       (kernels.hpp:189)
+  T pin_u[3];  // pin velocity                       (kernels.hpp:248-249)
+  int32_t plug_pressure;  // plugged AND pressure != 0 (kernels.hpp:183)
+  int32_t plug_gravity, plug_drag;
+  int32_t n_spheres, sphere0, n_planes, plane0;
+  int32_t n_pins;
+  int64_t pin_word0;  // first word of this cloth's pin bitmap / rank prefix
+  int64_t anchor0;    // first anchor (x3) of this cloth
+};
+
+template <typename T>
+struct SphereConst {
+  T c[3];
+  T R;
+  T Rband;  // R * (1 + 16 eps)          (kernels.hpp:217, contact_band :23-28)
+  T omf;    // 1 - friction              (kernels.hpp:221,239)
+};
+
+// Plane z = h, normal +z (extension; no reference counterpart).
+template <typename T>
+struct PlaneConst {
+  T h;
+  T band;  // max(|h|, 1) * 16 eps: velocity-level contact when x.z - h <= band
+  T omf;
+};
+
+struct Health {
+  // min over (frame << 32 | node) of non-finite cell impulses (net.cpp:139-140); ~0 if none
+  unsigned long long impulse_key;
+  int32_t state_frame;  // first frame with a non-finite x' or v' (eval.cpp:98-99); INT_MAX
+  int32_t pad;
+};
+
+template <typename T>
+struct StepArgs {
+  const T* in;
+  T* out;
+  int64_t plane_stride;  // elements per plane per cloth
+  int32_t pitch;
+  int32_t nx, ny;        // global grid
+  int32_t g0;            // global row of local row 0
+  int32_t u0, u1;        // global rows to update [u0, u1)
+  int32_t batch;
+  int32_t k;             // step index: t_next = T(k+1) * dt
+  int32_t use_t_override;
+  T t_override;
+  const ClothConst<T>* cloths;
+  const SphereConst<T>* spheres;
+  const PlaneConst<T>* planes;
+  const uint32_t* pin_bits;
+  const int32_t* pin_rank;  // prefix popcount per bitmap word
+  const T* pin_anchors;
+  uint8_t* constrained;     // [batch][ny*nx] global node index, or nullptr
+  T* impulse;               // planar [batch][3][local plane] or nullptr (forward-only output)
+  Health* health;           // [batch] or nullptr
+  NetConst<T> net;
+};
+
+// ---- shared per-node tail -----------------------------------------------------------------
+// plug_tail: gravity + drag of add_plug_impulse (kernels.hpp:188-195), applied after pressure.
+// advance_node: advance_with_impulse for one node (kernels.hpp:210-251).
+// Exactly the reference operation order, in non-contractible IEEE ops.
+template <typename T>
+__device__ __forceinline__ void plug_tail(const ClothConst<T>& cc, const T v[3], T imp[3]) {
+  using R = RN<T>;
+  if (cc.plug_gravity) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) imp[d] = R::add(imp[d], cc.dv[d]);
+  }
+  if (cc.plug_drag) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) imp[d] = R::sub(imp[d], R::mul(v[d], cc.drag_c));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothConst<T>& cc,
+                                             int64_t gnode, const T x[3], const T v[3],
+                                             const T imp[3], T xo[3], T vo[3], uint8_t& mask) {
+  using R = RN<T>;
+  mask = 0;
+  T vv[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) vv[d] = R::add(v[d], imp[d]);
+  // velocity-level response on the OLD positions (kernels.hpp:213-225)
+  for (int s = 0; s < cc.n_spheres; ++s) {
+    const SphereConst<T> sp = a.spheres[cc.sphere0 + s];
+    T r[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) r[d] = R::sub(x[d], sp.c[d]);
+    const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
+    if (dist > T(0) && dist <= sp.Rband) {
+      const T vn = R::div(R::add(R::add(R::mul(vv[0], r[0]), R::mul(vv[1], r[1])), R::mul(vv[2], r[2])), dist);
+      if (vn < T(0)) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const T nrm = R::div(r[d], dist);
+          vv[d] = R::mul(R::sub(vv[d], R::mul(nrm, vn)), sp.omf);
+        }
+        mask = 1;
+      }
+    }
+  }
+  for (int q = 0; q < cc.n_planes; ++q) {
+    const PlaneConst<T> pl = a.planes[cc.plane0 + q];
+    if (R::sub(x[2], pl.h) <= pl.band && vv[2] < T(0)) {
+      const T vn = vv[2];
+      vv[0] = R::mul(vv[0], pl.omf);
+      vv[1] = R::mul(vv[1], pl.omf);
+      vv[2] = R::mul(R::sub(vv[2], vn), pl.omf);
+      mask = 1;
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    vo[d] = vv[d];
+    xo[d] = R::add(x[d], R::mul(vv[d], cc.dt));
+  }
+  // position-level intersection elimination (kernels.hpp:229-244)
+  for (int s = 0; s < cc.n_spheres; ++s) {
+    const SphereConst<T> sp = a.spheres[cc.sphere0 + s];
+    T r[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) r[d] = R::sub(xo[d], sp.c[d]);
+    const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
+    if (dist > T(0) && dist < sp.R) {
+      T nrm[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        nrm[d] = R::div(r[d], dist);
+        xo[d] = R::add(sp.c[d], R::mul(nrm[d], sp.R));
+      }
+      const T vn = R::add(R::add(R::mul(vo[0], nrm[0]), R::mul(vo[1], nrm[1])), R::mul(vo[2], nrm[2]));
+      if (vn < T(0)) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) vo[d] = R::mul(R::sub(vo[d], R::mul(nrm[d], vn)), sp.omf);
+      }
+      mask = 1;
+    }
+  }
+  for (int q = 0; q < cc.n_planes; ++q) {
+    const PlaneConst<T> pl = a.planes[cc.plane0 + q];
+    if (xo[2] < pl.h) {
+      xo[2] = pl.h;
+      const T vn = vo[2];
+      if (vn < T(0)) {
+        vo[0] = R::mul(vo[0], pl.omf);
+        vo[1] = R::mul(vo[1], pl.omf);
+        vo[2] = R::mul(R::sub(vo[2], vn), pl.omf);
+      }
+      mask = 1;
+    }
+  }
+  // Dirichlet re-pin last (kernels.hpp:245-251): bitmap + rank prefix -> anchor slot
+  if (cc.n_pins > 0) {
+    const int64_t w = cc.pin_word0 + (gnode >> 5);
+    const uint32_t bits = __ldg(a.pin_bits + w);
+    const uint32_t bit = 1u << (gnode & 31);
+    if (bits & bit) {
+      const int64_t slot = cc.anchor0 + __ldg(a.pin_rank + w) + __popc(bits & (bit - 1u));
+      const T t_next = a.use_t_override ? a.t_override : R::mul(T(a.k + 1), cc.dt);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        vo[d] = cc.pin_u[d];
+        xo[d] = R::add(__ldg(a.pin_anchors + 3 * slot + d), R::mul(cc.pin_u[d], t_next));
+      }
+      mask = 1;
+    }
+  }
+}
+
+// ---- pressure plug (accumulate_pressure kernels.hpp:142-155 + scaling :183-187) -----------
+// e,n,w,s are x_i - x_{E,N,W,S}; only interior nodes get the cross products, the others a
+// zero force; the reference then adds f*scale to every node.
+template <typename T>
+__device__ __forceinline__ void pressure_plug(const ClothConst<T>& cc, bool interior,
+                                              const T e[3], const T n[3], const T w[3],
+                                              const T s[3], T imp[3]) {
+  using R = RN<T>;
+  T f[3] = {T(0), T(0), T(0)};
+  if (interior) {
+    auto cross = [](const T* p, const T* q, T* o) {
+      o[0] = R::sub(R::mul(p[1], q[2]), R::mul(p[2], q[1]));
+      o[1] = R::sub(R::mul(p[2], q[0]), R::mul(p[0], q[2]));
+      o[2] = R::sub(R::mul(p[0], q[1]), R::mul(p[1], q[0]));
+    };
+    T c1[3], c2[3], c3[3], c4[3];
+    cross(e, n, c1);
+    cross(n, w, c2);
+    cross(w, s, c3);
+    cross(s, e, c4);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[d] = R::mul(R::add(R::add(R::add(c1[d], c2[d]), c3[d]), c4[d]), cc.pressure);
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) imp[d] = R::add(imp[d], R::mul(f[d], cc.scale));
+}
+
+}  // namespace scb

@@ -1,0 +1,51 @@
+// Launch interface between the C-ABI layer (capi.cu) and the kernel translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "sc_device.cuh"
+
+namespace scb {
+
+enum { KIND_STEP = 0, KIND_FORWARD = 1, KIND_PLUG = 2, KIND_ADVANCE = 3 };
+
+// parity_kernels.cu (compiled with --fmad=false)
+template <typename T>
+cudaError_t launch_parity(const StepArgs<T>& a, int kind, cudaStream_t stream);
+
+// fast_kernels.cu: f32 FAST step (FMA, rsqrt ISRU, one ISRU per undirected edge).
+// Gains folded into the weights: wL' = g wL, wN' = g wN, wD' = g^2 wD, alpha' = alpha g^2.
+struct FastNet {
+  float wl[kChannels], wn[kChannels], wd[kChannels];
+  float nwl[kChannels], nwn[kChannels];  // negated, for the far endpoint of an edge
+  float alpha[kChannels];
+  float b[3];
+  float wv;
+  int alpha1;  // every alpha' == 1 (default gains and alpha): skips one multiply per edge
+};
+struct FastPlan {
+  int n_strips, seg_rows, n_segs;
+  int64_t units;  // one single-warp CTA per (cloth, 128-column strip, row segment)
+  size_t smem;
+};
+FastNet make_fast_net(const NetConst<float>& net);
+// Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
+bool fast_supported(const NetConst<float>& net);
+FastPlan plan_fast(int nx, int rows, int batch, int device);
+// tmap: 3-D tensor map over a.in, dims (pitch, local rows, 6*batch), box (132, 1, 6).
+cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
+                        const FastPlan& plan, cudaStream_t stream);
+
+// layout.cu: AoS [batch][node][3] <-> planar [batch][6][rows][pitch]
+// (rows = the ctx's local rows; AoS arrays hold exactly those rows.)
+template <typename T>
+cudaError_t launch_aos_to_planar(const T* x_aos, const T* v_aos, T* planar, int batch, int nx,
+                                 int rows, int64_t plane_stride, int pitch, cudaStream_t stream);
+template <typename T>
+cudaError_t launch_planar_to_aos(const T* planar, T* x_aos, T* v_aos, int batch, int nx, int rows,
+                                 int64_t plane_stride, int pitch, cudaStream_t stream);
+
+}  // namespace scb
