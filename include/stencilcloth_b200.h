@@ -141,6 +141,10 @@ sc_status sc_ctx_sync(sc_ctx* ctx);
  * net.cpp:30-51 and eval.cpp:98-99). Any of the outputs may be NULL. */
 sc_status sc_ctx_get_health(sc_ctx* ctx, int32_t* first_bad_impulse_frame,
                             int32_t* first_bad_impulse_node, int32_t* first_bad_state_frame);
+/* Non-finite tracking during device-resident stepping (sc_ctx_advance / sc_rollout*): on by
+ * default for SC_F64 contexts (rollout's checks, eval.cpp:98-99, net.cpp:139-140), off for
+ * SC_F32 (run_steps<float> checks nothing, eval.cpp:48-59). Per-operator calls always track. */
+sc_status sc_ctx_set_health_checks(sc_ctx* ctx, int32_t on);
 
 /* Host-to-host rollout: upload x0/v0, advance `steps`, download the final state. When
  * `constrained` is non-NULL it receives the mask of the LAST step ([batch][node] uint8, the

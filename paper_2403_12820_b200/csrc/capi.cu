@@ -127,6 +127,7 @@ struct sc_ctx {
   CUtensorMap tmap[2];
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
+  bool health_on = false;  // non-finite tracking in device-resident stepping
 
   size_t elem() const { return prec == SC_F32 ? 4 : 8; }
   int64_t nodes_global() const { return static_cast<int64_t>(nx) * ny; }
@@ -483,11 +484,11 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
     const int k = k0 + s;
     uint8_t* m = (s == steps - 1) ? dev_mask_last : nullptr;
     if (c->prec == SC_F32)
-      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr, c->health.p, c->u0, c->u1,
-                        c->stream);
+      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr,
+                        c->health_on ? c->health.p : nullptr, c->u0, c->u1, c->stream);
     else
-      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr, c->health.p, c->u0,
-                         c->u1, c->stream);
+      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr,
+                         c->health_on ? c->health.p : nullptr, c->u0, c->u1, c->stream);
     c->cur = 1 - c->cur;
   }
 }
@@ -521,6 +522,7 @@ sc_status sc_ctx_create(int device, sc_precision precision, sc_ctx** out) {
     auto* c = new sc_ctx();
     c->device = device;
     c->prec = precision;
+    c->health_on = precision == SC_F64;  // the reference's f64 rollout checks; run_steps<float> does not
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreate(&c->ev0), "cudaEventCreate");
     ck(cudaEventCreate(&c->ev1), "cudaEventCreate");
@@ -602,7 +604,7 @@ sc_status sc_ctx_set_params(sc_ctx* c, const sc_params* p) {
     c->net32 = make_net<float>(p);
     c->net64 = make_net<double>(p);
     c->fast = make_fast_net(c->net32);
-    c->fast_ok = fast_supported(c->net32);
+    c->fast_ok = fast_supported(c->net32, c->nx);
     c->has_params = true;
   });
 }
@@ -630,6 +632,13 @@ sc_status sc_ctx_advance(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mode) {
     require_ready(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     advance_impl(c, steps, k0, mode, nullptr);
+  });
+}
+
+sc_status sc_ctx_set_health_checks(sc_ctx* c, int32_t on) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    c->health_on = on != 0;
   });
 }
 

@@ -69,28 +69,142 @@ __device__ __forceinline__ void tma_load_row(float* dst, const CUtensorMap* map,
       : "memory");
 }
 
+// rsqrt without the denormal fix-up rsqrtf() carries under -ftz=false: q = 1 + a dx^2 >= 1.
+__device__ __forceinline__ float rsqrt_q(float q) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+  return r;
+}
+
 // Edge contribution to its origin node a (channel ca) and far node b (channel cb = -ca):
 //   a: acc += dx*wL'_ca + s*(wN'_ca + dv*wD'_ca)
 //   b: acc += dx*(-wL'_cb) + s*(dv*wD'_cb - wN'_cb)
 // with dx = x_a - x_b, dv = v_a - v_b, s = dx * rsqrt(1 + alpha'_c dx^2) and the gains folded
 // into the primed weights (wL' = g wL, wN' = g wN, wD' = g^2 wD, alpha' = alpha g^2).
-template <bool ALPHA1>
-__device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, float xa, float xb,
-                                     float va, float vb, bool push_a, bool push_b, float& acc_a,
-                                     float& acc_b) {
-  const float dx = xa - xb;
-  const float dv = va - vb;
+// Invalid edges (an endpoint outside the grid) arrive with dx = dv = 0 and contribute exactly 0.
+template <bool ALPHA1, bool PA, bool PB>
+__device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, float dx, float dv,
+                                     float& acc_a, float& acc_b) {
   const float q = ALPHA1 ? fmaf(dx, dx, 1.0f) : fmaf(dx * f.alpha[ca], dx, 1.0f);
-  const float s = dx * rsqrtf(q);
-  if (push_a) {
+  const float s = dx * rsqrt_q(q);
+  if (PA) {
     const float t = fmaf(dv, f.wd[ca], f.wn[ca]);
     acc_a = fmaf(dx, f.wl[ca], acc_a);
     acc_a = fmaf(s, t, acc_a);
   }
-  if (push_b) {
+  if (PB) {
     const float t = fmaf(dv, f.wd[cb], f.nwn[cb]);
     acc_b = fmaf(dx, f.nwl[cb], acc_b);
     acc_b = fmaf(s, t, acc_b);
+  }
+}
+
+// Lane window of a staged row: columns ix0-2 .. ix0+5 <-> box index 4*lane+2 .. 4*lane+9.
+__device__ __forceinline__ void load8(const float* base, int lane, float* o) {
+  const float2 l = *reinterpret_cast<const float2*>(base + FW * lane + 2);
+  const float4 m = *reinterpret_cast<const float4*>(base + FW * lane + 4);
+  const float2 r = *reinterpret_cast<const float2*>(base + FW * lane + 8);
+  o[0] = l.x; o[1] = l.y; o[2] = m.x; o[3] = m.y; o[4] = m.z; o[5] = m.w; o[6] = r.x; o[7] = r.y;
+}
+
+__device__ __forceinline__ void load4(const float* base, int lane, float* o) {
+  const float4 m = *reinterpret_cast<const float4*>(base + FW * lane + 4);
+  o[0] = m.x; o[1] = m.y; o[2] = m.z; o[3] = m.w;
+}
+
+// All edges of one component whose upper endpoint lies on row R, pushed into the accumulators
+// of rows R-2 (A0), R-1 (A1), R (A2). mL / mRt zero the edges that leave the grid through the
+// strip's left / right boundary lane; GENERAL additionally applies the row masks of the first
+// and last two rows of the cloth (uniform per step).
+template <bool ALPHA1, bool GENERAL>
+__device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, const float* row1,
+                                          const float* row2, int lane, float mL, float mRt,
+                                          float mR, float m1, float m2, float (&A0)[4],
+                                          float (&A1)[4], float (&A2)[4], int d) {
+  float xr[8], vr[8], x1[8], v1[8], x2[4], v2[4];
+  load8(rowR + d * BOXW, lane, xr);
+  load8(rowR + (3 + d) * BOXW, lane, vr);
+  load8(row1 + d * BOXW, lane, x1);
+  load8(row1 + (3 + d) * BOXW, lane, v1);
+  load4(row2 + d * BOXW, lane, x2);
+  load4(row2 + (3 + d) * BOXW, lane, v2);
+  // init row R: b + v*wV
+#pragma unroll
+  for (int k = 0; k < 4; ++k) A2[k] = fmaf(vr[k + 2], f.wv, f.b[d]);
+
+  float dummy = 0.0f;
+  auto mask_of = [&](int e, int lo, int hi, float row) -> float {
+    // lane-column mask for slot e of an edge family whose slots < lo / > hi may leave the grid
+    float m = e < lo ? mL : (e > hi ? mRt : 1.0f);
+    return GENERAL ? m * row : m;
+  };
+  // E edges in row R: a = col ix0-1+e (j = e+1), b = col ix0+e (j = e+2)
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = xr[e + 1] - xr[e + 2], dv = vr[e + 1] - vr[e + 2];
+    if (GENERAL || e == 0 || e == 4) {
+      const float m = mask_of(e, 1, 3, mR);
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, A2[0]);
+    else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, A2[3], dummy);
+    else edge<ALPHA1, true, true>(f, 0, 2, dx, dv, A2[e - 1 < 0 ? 0 : e - 1], A2[e > 3 ? 3 : e]);
+  }
+  // E2 edges in row R: a = col ix0-2+e (j = e), b = col ix0+e (j = e+2)
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    float dx = xr[e] - xr[e + 2], dv = vr[e] - vr[e + 2];
+    if (GENERAL || e <= 1 || e >= 4) {
+      const float m = mask_of(e, 2, 3, mR);
+      dx *= m;
+      dv *= m;
+    }
+    if (e <= 1) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy, A2[e]);
+    else if (e >= 4) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[e - 2], dummy);
+    else edge<ALPHA1, true, true>(f, 8, 10, dx, dv, A2[e - 2], A2[e]);
+  }
+  // N edges (R-1 -> R) and N2 edges (R-2 -> R), owned columns
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float dx = x1[k + 2] - xr[k + 2], dv = v1[k + 2] - vr[k + 2];
+    if (GENERAL) {
+      dx *= m1;
+      dv *= m1;
+    }
+    edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[k], A2[k]);
+    float dx2 = x2[k] - xr[k + 2], dv2 = v2[k] - vr[k + 2];
+    if (GENERAL) {
+      dx2 *= m2;
+      dv2 *= m2;
+    }
+    edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[k], A2[k]);
+  }
+  // NE edges: a = (ix0-1+e, R-1) (j = e+1), b = (ix0+e, R) (j = e+2)
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = x1[e + 1] - xr[e + 2], dv = v1[e + 1] - vr[e + 2];
+    if (GENERAL || e == 0 || e == 4) {
+      const float m = mask_of(e, 1, 3, m1);
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, A2[0]);
+    else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[3], dummy);
+    else edge<ALPHA1, true, true>(f, 4, 6, dx, dv, A1[e - 1 < 0 ? 0 : e - 1], A2[e > 3 ? 3 : e]);
+  }
+  // NW edges: a = (ix0+e, R-1) (j = e+2), b = (ix0+e-1, R) (j = e+1)
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = x1[e + 2] - xr[e + 1], dv = v1[e + 2] - vr[e + 1];
+    if (GENERAL || e == 0 || e == 4) {
+      const float m = mask_of(e, 1, 3, m1);
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[0], dummy);
+    else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, A2[3]);
+    else edge<ALPHA1, true, true>(f, 5, 7, dx, dv, A1[e > 3 ? 3 : e], A2[e - 1 < 0 ? 0 : e - 1]);
   }
 }
 
@@ -99,8 +213,9 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
                                                       const int n_segs) {
-  extern __shared__ __align__(128) float ring[];  // [RING][6][BOXW]
+  extern __shared__ __align__(128) float ring[];  // [RING][6][BOXW] (slot stride ROWF)
   __shared__ __align__(8) uint64_t full[RING];
+  __shared__ float scratch[32][13];  // per-lane impulse staging for the collider finish
 
   const int lane = threadIdx.x;
   const int unit = blockIdx.x;
@@ -133,34 +248,23 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     if (r_first + 1 <= r_last) issue(r_first + 1);
   }
 
-  // lane-constant edge validity (both endpoints inside the grid columns)
-  bool vE[5], vE2[6], vNE[5], vNW[5];
-#pragma unroll
-  for (int e = 0; e < 5; ++e) {
-    const int c = ix0 - 1 + e;
-    vE[e] = c >= 0 && c + 1 < nx;
-    vNE[e] = c >= 0 && c + 1 < nx;
-    const int cw = ix0 + e;
-    vNW[e] = cw - 1 >= 0 && cw < nx;
-  }
-#pragma unroll
-  for (int e = 0; e < 6; ++e) {
-    const int c = ix0 - 2 + e;
-    vE2[e] = c >= 0 && c + 2 < nx;
-  }
-  bool vN[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) vN[k] = ix0 + k < nx;
+  // nx % 4 == 0 (fast_supported): only a strip's outermost lanes own edges leaving the grid
+  const float mL = ix0 >= 1 ? 1.0f : 0.0f;
+  const float mRt = ix0 + 4 < nx ? 1.0f : 0.0f;
+  const bool lane_live = ix0 < nx;
 
   const ClothConst<float> cc = a.cloths[b];
+  const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
+                      a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
   float* out_b = a.out + static_cast<int64_t>(b) * 6 * a.plane_stride;
+  const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
 
-  float A0[4][3], A1[4][3], A2[4][3];  // rows R-2, R-1, R
+  float A0[3][4], A1[3][4], A2[3][4];  // [component][column] for rows R-2, R-1, R
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int d = 0; d < 3; ++d)
 #pragma unroll
-    for (int d = 0; d < 3; ++d) A0[k][d] = A1[k][d] = A2[k][d] = 0.0f;
+    for (int k = 0; k < 4; ++k) A0[d][k] = A1[d][k] = A2[d][k] = 0.0f;
 
 #pragma unroll 1
   for (int R = r_first; R <= r_last; ++R) {
@@ -175,171 +279,151 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     const float* rowR = ring + (t % RING) * ROWF;
     const float* row1 = ring + ((t + RING - 1) % RING) * ROWF;
     const float* row2 = ring + ((t + RING - 2) % RING) * ROWF;
-    const bool okR = R >= 0 && R < ny;
-    const bool ok1 = okR && R - 1 >= 0;  // rows R-1 and R both in the grid
-    const bool ok2 = okR && R - 2 >= 0;  // rows R-2 and R both in the grid
-    const bool have1 = t >= 1, have2 = t >= 2;
-
+    if (R - 2 >= 0 && R < ny) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      // row R and R-1: columns ix0-2 .. ix0+5 <-> box index 4*lane+2 .. 4*lane+9
-      // (LDS.64 + LDS.128 + LDS.64); row R-2: columns ix0 .. ix0+3 (one LDS.128)
-      float xr[8], vr[8], x1[8], v1[8], x2[8], v2[8];
-      auto load8 = [&](const float* base, float* o) {
-        const float2 l = *reinterpret_cast<const float2*>(base + FW * lane + 2);
-        const float4 m = *reinterpret_cast<const float4*>(base + FW * lane + 4);
-        const float2 r = *reinterpret_cast<const float2*>(base + FW * lane + 8);
-        o[0] = l.x; o[1] = l.y; o[2] = m.x; o[3] = m.y; o[4] = m.z; o[5] = m.w; o[6] = r.x; o[7] = r.y;
-      };
-      load8(rowR + d * BOXW, xr);
-      load8(rowR + (3 + d) * BOXW, vr);
-      if (have1) {
-        load8(row1 + d * BOXW, x1);
-        load8(row1 + (3 + d) * BOXW, v1);
-      } else {
+      for (int d = 0; d < 3; ++d)
+        comp_pass<ALPHA1, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f, A0[d], A1[d],
+                                 A2[d], d);
+    } else {
+      const bool okR = R >= 0 && R < ny;
+      const float mR = okR ? 1.f : 0.f;
+      const float m1 = (okR && R - 1 >= 0) ? 1.f : 0.f;
+      const float m2 = (okR && R - 2 >= 0) ? 1.f : 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x1[j] = v1[j] = 0.0f;
-      }
-      if (have2) {
-        const float4 a0 = *reinterpret_cast<const float4*>(row2 + d * BOXW + FW * lane + 4);
-        const float4 c0 = *reinterpret_cast<const float4*>(row2 + (3 + d) * BOXW + FW * lane + 4);
-        x2[2] = a0.x; x2[3] = a0.y; x2[4] = a0.z; x2[5] = a0.w;
-        v2[2] = c0.x; v2[3] = c0.y; v2[4] = c0.z; v2[5] = c0.w;
-      } else {
-#pragma unroll
-        for (int j = 2; j < 6; ++j) x2[j] = v2[j] = 0.0f;
-      }
-      // init row R: b + v*wV
-#pragma unroll
-      for (int k = 0; k < 4; ++k) A2[k][d] = fmaf(vr[k + 2], f.wv, f.b[d]);
-
-      float dummy = 0.0f;
-      // E edges in row R: a = col ix0-1+e (box j = e+1), b = col ix0+e (j = e+2)
-#pragma unroll
-      for (int e = 0; e < 5; ++e) {
-        float& acc_a = e >= 1 ? A2[e >= 1 ? e - 1 : 0][d] : dummy;
-        float& acc_b = e <= 3 ? A2[e <= 3 ? e : 0][d] : dummy;
-        edge<ALPHA1>(f, 0, 2, xr[e + 1], xr[e + 2], vr[e + 1], vr[e + 2], okR && vE[e] && e >= 1,
-                     okR && vE[e] && e <= 3, acc_a, acc_b);
-      }
-      // E2 edges in row R: a = col ix0-2+e (j = e), b = col ix0+e (j = e+2)
-#pragma unroll
-      for (int e = 0; e < 6; ++e) {
-        float& acc_a = e >= 2 ? A2[e >= 2 ? e - 2 : 0][d] : dummy;
-        float& acc_b = e <= 3 ? A2[e <= 3 ? e : 0][d] : dummy;
-        edge<ALPHA1>(f, 8, 10, xr[e], xr[e + 2], vr[e], vr[e + 2], okR && vE2[e] && e >= 2,
-                     okR && vE2[e] && e <= 3, acc_a, acc_b);
-      }
-      // N edges (R-1 -> R) and N2 edges (R-2 -> R), owned columns
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        edge<ALPHA1>(f, 1, 3, x1[k + 2], xr[k + 2], v1[k + 2], vr[k + 2], ok1 && vN[k],
-                     ok1 && vN[k], A1[k][d], A2[k][d]);
-        edge<ALPHA1>(f, 9, 11, x2[k + 2], xr[k + 2], v2[k + 2], vr[k + 2], ok2 && vN[k],
-                     ok2 && vN[k], A0[k][d], A2[k][d]);
-      }
-      // NE edges: a = (ix0-1+e, R-1) (j = e+1), b = (ix0+e, R) (j = e+2)
-#pragma unroll
-      for (int e = 0; e < 5; ++e) {
-        float& acc_a = e >= 1 ? A1[e >= 1 ? e - 1 : 0][d] : dummy;
-        float& acc_b = e <= 3 ? A2[e <= 3 ? e : 0][d] : dummy;
-        edge<ALPHA1>(f, 4, 6, x1[e + 1], xr[e + 2], v1[e + 1], vr[e + 2], ok1 && vNE[e] && e >= 1,
-                     ok1 && vNE[e] && e <= 3, acc_a, acc_b);
-      }
-      // NW edges: a = (ix0+e, R-1) (j = e+2), b = (ix0+e-1, R) (j = e+1)
-#pragma unroll
-      for (int e = 0; e < 5; ++e) {
-        float& acc_a = e <= 3 ? A1[e <= 3 ? e : 0][d] : dummy;
-        float& acc_b = e >= 1 ? A2[e >= 1 ? e - 1 : 0][d] : dummy;
-        edge<ALPHA1>(f, 5, 7, x1[e + 2], xr[e + 1], v1[e + 2], vr[e + 1], ok1 && vNW[e] && e <= 3,
-                     ok1 && vNW[e] && e >= 1, acc_a, acc_b);
-      }
+      for (int d = 0; d < 3; ++d)
+        comp_pass<ALPHA1, true>(f, rowR, row1, row2, lane, mL, mRt, mR, m1, m2, A0[d], A1[d],
+                                A2[d], d);
     }
 
     // row R-2 is complete: plug, integrate, collide, pin, store
     const int Rf = R - 2;
-    if (Rf >= y0 && Rf < y1) {
-      const float* rowf = row2;
-      float xs[4][3], vs[4][3];
+    if (Rf >= y0 && Rf < y1 && lane_live) {
+      float xs[3][4], vs[3][4];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const float4 p = *reinterpret_cast<const float4*>(rowf + d * BOXW + FW * lane + 4);
-        const float4 q = *reinterpret_cast<const float4*>(rowf + (3 + d) * BOXW + FW * lane + 4);
-        xs[0][d] = p.x; xs[1][d] = p.y; xs[2][d] = p.z; xs[3][d] = p.w;
-        vs[0][d] = q.x; vs[1][d] = q.y; vs[2][d] = q.z; vs[3][d] = q.w;
+        load4(row2 + d * BOXW, lane, xs[d]);
+        load4(row2 + (3 + d) * BOXW, lane, vs[d]);
       }
-      float xo[4][3], vo[4][3];
-      uint8_t mk[4];
+      float xo[3][4], vo[3][4];
+      if (simple) {
+        // add_plug_impulse gravity/drag + advance without colliders, IEEE-exact like PARITY
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int ix = ix0 + k;
-        const int64_t gnode = static_cast<int64_t>(Rf) * nx + ix;
-        float imp[3] = {A0[k][0], A0[k][1], A0[k][2]};
-        if (a.health && ix < nx && !(isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]))) {
-          const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
-                                         static_cast<unsigned long long>(gnode);
-          atomicMin(&a.health[b].impulse_key, key);
-        }
-        if (cc.plug_pressure) {
-          const float* rs = ring + ((t + RING - 3) % RING) * ROWF;  // row Rf-1
-          const float* rn = row1;                                   // row Rf+1
-          const int j = FW * lane + 4 + k;
-          const bool interior = ix >= 1 && ix <= nx - 2 && Rf >= 1 && Rf <= ny - 2;
-          float e[3], n[3], w[3], s[3];
+        for (int k = 0; k < 4; ++k) {
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            e[d] = __fsub_rn(xs[k][d], rowf[d * BOXW + j + 1]);
-            n[d] = __fsub_rn(xs[k][d], rn[d * BOXW + j]);
-            w[d] = __fsub_rn(xs[k][d], rowf[d * BOXW + j - 1]);
-            s[d] = __fsub_rn(xs[k][d], rs[d * BOXW + j]);
+            float imp = A0[d][k];
+            if (cc.plug_gravity) imp = __fadd_rn(imp, cc.dv[d]);
+            if (cc.plug_drag) imp = __fsub_rn(imp, __fmul_rn(vs[d][k], cc.drag_c));
+            const float vv = __fadd_rn(vs[d][k], imp);
+            vo[d][k] = vv;
+            xo[d][k] = __fadd_rn(xs[d][k], __fmul_rn(vv, cc.dt));
           }
-          pressure_plug(cc, interior, e, n, w, s, imp);
         }
-        plug_tail(cc, vs[k], imp);
-        advance_node(a, cc, gnode, xs[k], vs[k], imp, xo[k], vo[k], mk[k]);
-      }
-      float* o = out_b + static_cast<int64_t>(Rf - a.g0) * a.pitch + ix0;
-      if (ix0 + 3 < nx) {
+        if (cc.n_pins > 0) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int64_t gnode = static_cast<int64_t>(Rf) * nx + ix0 + k;
+            const int64_t w = cc.pin_word0 + (gnode >> 5);
+            const uint32_t bits = __ldg(a.pin_bits + w);
+            const uint32_t bit = 1u << (gnode & 31);
+            if (bits & bit) {
+              const int64_t slot = cc.anchor0 + __ldg(a.pin_rank + w) + __popc(bits & (bit - 1u));
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                vo[d][k] = cc.pin_u[d];
+                xo[d][k] = __fadd_rn(__ldg(a.pin_anchors + 3 * slot + d),
+                                     __fmul_rn(cc.pin_u[d], t_next));
+              }
+            }
+          }
+        }
+        if (a.health) {
+          bool fin_imp = true, fin = true;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              fin_imp = fin_imp && isfinite(A0[d][k]);
+              fin = fin && isfinite(xo[d][k]) && isfinite(vo[d][k]);
+            }
+          if (!fin_imp) {
+            for (int k = 0; k < 4; ++k)
+              if (!(isfinite(A0[0][k]) && isfinite(A0[1][k]) && isfinite(A0[2][k]))) {
+                const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
+                                               static_cast<unsigned long long>(Rf * nx + ix0 + k);
+                atomicMin(&a.health[b].impulse_key, key);
+                break;
+              }
+          }
+          if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
+        }
+        float* o = out_b + static_cast<int64_t>(Rf - a.g0) * a.pitch + ix0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           *reinterpret_cast<float4*>(o + d * a.plane_stride) =
-              make_float4(xo[0][d], xo[1][d], xo[2][d], xo[3][d]);
+              make_float4(xo[d][0], xo[d][1], xo[d][2], xo[d][3]);
           *reinterpret_cast<float4*>(o + (3 + d) * a.plane_stride) =
-              make_float4(vo[0][d], vo[1][d], vo[2][d], vo[3][d]);
+              make_float4(vo[d][0], vo[d][1], vo[d][2], vo[d][3]);
         }
       } else {
+        // colliders / pressure / mask: one node at a time (compact code, same IEEE-exact chain)
+        const float* rs = ring + ((t + RING - 3) % RING) * ROWF;  // row Rf-1
 #pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) scratch[lane][d * 4 + k] = A0[d][k];  // own row only
+        float* o = out_b + static_cast<int64_t>(Rf - a.g0) * a.pitch;
+#pragma unroll 1
         for (int k = 0; k < 4; ++k) {
-          if (ix0 + k >= nx) break;
+          const int ix = ix0 + k;
+          const int j = FW * lane + 4 + k;
+          const int64_t gnode = static_cast<int64_t>(Rf) * nx + ix;
+          float px[3], pv[3], imp[3], po[3], qo[3];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            o[d * a.plane_stride + k] = xo[k][d];
-            o[(3 + d) * a.plane_stride + k] = vo[k][d];
+            px[d] = row2[d * BOXW + j];
+            pv[d] = row2[(3 + d) * BOXW + j];
+            imp[d] = scratch[lane][d * 4 + k];
           }
+          if (a.health && !(isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]))) {
+            const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
+                                           static_cast<unsigned long long>(gnode);
+            atomicMin(&a.health[b].impulse_key, key);
+          }
+          if (cc.plug_pressure) {
+            const bool interior = ix >= 1 && ix <= nx - 2 && Rf >= 1 && Rf <= ny - 2;
+            float e[3], n[3], w[3], sv[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              e[d] = __fsub_rn(px[d], row2[d * BOXW + j + 1]);
+              n[d] = __fsub_rn(px[d], row1[d * BOXW + j]);
+              w[d] = __fsub_rn(px[d], row2[d * BOXW + j - 1]);
+              sv[d] = __fsub_rn(px[d], rs[d * BOXW + j]);
+            }
+            pressure_plug(cc, interior, e, n, w, sv, imp);
+          }
+          plug_tail(cc, pv, imp);
+          uint8_t mk;
+          advance_node(a, cc, gnode, px, pv, imp, po, qo, mk);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            o[d * a.plane_stride + ix] = po[d];
+            o[(3 + d) * a.plane_stride + ix] = qo[d];
+          }
+          if (a.constrained) a.constrained[b * nodes + gnode] = mk;
+          if (a.health && !(isfinite(po[0]) && isfinite(po[1]) && isfinite(po[2]) &&
+                            isfinite(qo[0]) && isfinite(qo[1]) && isfinite(qo[2])))
+            atomicMin(&a.health[b].state_frame, a.k + 1);
         }
-      }
-      if (a.constrained) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (ix0 + k < nx) a.constrained[b * nodes + static_cast<int64_t>(Rf) * nx + ix0 + k] = mk[k];
-      }
-      if (a.health) {
-        bool fin = true;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            fin = fin && (ix0 + k >= nx || (isfinite(xo[k][d]) && isfinite(vo[k][d])));
-        if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
       }
     }
     // rotate accumulator rows
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        A0[k][d] = A1[k][d];
-        A1[k][d] = A2[k][d];
+      for (int k = 0; k < 4; ++k) {
+        A0[d][k] = A1[d][k];
+        A1[d][k] = A2[d][k];
       }
   }
 }
@@ -365,7 +449,8 @@ FastNet make_fast_net(const NetConst<float>& n) {
   return f;
 }
 
-bool fast_supported(const NetConst<float>& net) {
+bool fast_supported(const NetConst<float>& net, int nx) {
+  if (nx % 4 != 0) return false;  // the strip column masks assume whole float4 columns
   static const int neg[kChannels] = {2, 3, 0, 1, 6, 7, 4, 5, 10, 11, 8, 9};
   for (int c = 0; c < kChannels; ++c)
     if (net.gain[c] != net.gain[neg[c]]) return false;

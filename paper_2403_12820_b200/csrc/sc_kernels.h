@@ -33,9 +33,9 @@ struct FastPlan {
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
-bool fast_supported(const NetConst<float>& net);
+bool fast_supported(const NetConst<float>& net, int nx);
 FastPlan plan_fast(int nx, int rows, int batch, int device);
-// tmap: 3-D tensor map over a.in, dims (pitch, local rows, 6*batch), box (132, 1, 6).
+// tmap: 3-D tensor map over a.in, dims (pitch, local rows, 6*batch), box (136, 1, 6).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
                         const FastPlan& plan, cudaStream_t stream);
 
