@@ -174,6 +174,10 @@ sc_status sc_nn_step(sc_ctx* ctx, const void* x, const void* v, double t_next, s
  * timed steps from the ctx state, timed with CUDA events on the ctx stream. */
 sc_status sc_benchmark(sc_ctx* ctx, int32_t steps, int32_t warmup, sc_mode mode,
                        double* seconds);
+/* Per-launch device time of `steps` consecutive fused steps (events between launches on the
+ * ctx stream), for roofline accounting: launch_ms[steps]. */
+sc_status sc_benchmark_launches(sc_ctx* ctx, int32_t steps, int32_t k0, sc_mode mode,
+                                float* launch_ms);
 
 /* ---- row-strip domain decomposition (one rank's strip of a tall cloth) ------------------ */
 /* Restricts the ctx to global rows [row0, row0 + rows) of an ny-row cloth plus up to two ghost

@@ -91,6 +91,7 @@ SIGNATURES = {
     "sc_advance_with_impulse": (C.c_int, [_P, _P, _P, _P, C.c_double, _P, _P, _P]),
     "sc_nn_step": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, _P, _P, _P]),
     "sc_benchmark": (C.c_int, [_P, _I, _I, C.c_int, C.POINTER(C.c_double)]),
+    "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),
     "sc_ctx_halo_elems": (C.c_int64, [_P]),
     "sc_ctx_halo_pack": (C.c_int, [_P, _I, _P, _P]),

@@ -197,6 +197,12 @@ class Context:
                                                C.byref(sec)))
         return sec.value
 
+    def benchmark_launches(self, steps: int, k0: int = 0, mode: str = "fast") -> np.ndarray:
+        ms = np.zeros(int(steps), np.float32)
+        _raise(self.lib, self.lib.sc_benchmark_launches(self.h, int(steps), int(k0), MODES[mode],
+                                                        _ptr(ms)))
+        return ms
+
     def launch_count(self) -> int:
         return int(self.lib.sc_ctx_launch_count(self.h))
 

@@ -827,6 +827,28 @@ sc_status sc_benchmark(sc_ctx* c, int32_t steps, int32_t warmup, sc_mode mode, d
   });
 }
 
+sc_status sc_benchmark_launches(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mode,
+                                float* launch_ms) {
+  return guarded([&] {
+    require_ready(c);
+    if (steps < 1) throw_config("bench: steps must be >= 1");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(steps) + 1);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    ck(cudaEventRecord(ev[0], c->stream), "event");
+    for (int s = 0; s < steps; ++s) {
+      advance_impl(c, 1, k0 + s, mode, nullptr);
+      ck(cudaEventRecord(ev[static_cast<size_t>(s) + 1], c->stream), "event");
+    }
+    ck(cudaEventSynchronize(ev.back()), "event sync");
+    for (int s = 0; s < steps; ++s)
+      ck(cudaEventElapsedTime(&launch_ms[s], ev[static_cast<size_t>(s)],
+                              ev[static_cast<size_t>(s) + 1]),
+         "event time");
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
 int64_t sc_ctx_halo_elems(sc_ctx* c) { return c ? static_cast<int64_t>(6) * 2 * c->nx : 0; }
 
 }  // extern "C"

@@ -30,7 +30,7 @@ namespace {
 constexpr int FW = 4;              // columns per lane
 constexpr int STRIP = 32 * FW;     // columns per warp
 constexpr int BOXW = STRIP + 8;    // staged columns x0-4 .. x0+131 (2-column halo + alignment)
-constexpr int RING = 6;            // staged rows: R-3 .. R+2
+constexpr int RING = 5;            // staged rows: R-3 .. R+1 (one row of prefetch)
 constexpr int ROW_BYTES = 6 * BOXW * 4;            // bytes one TMA box delivers (6 planes)
 constexpr int ROWF = ((ROW_BYTES + 127) / 128) * 32;  // ring slot stride in floats (128 B aligned)
 
@@ -116,7 +116,7 @@ __device__ __forceinline__ void load4(const float* base, int lane, float* o) {
 // of rows R-2 (A0), R-1 (A1), R (A2). mL / mRt zero the edges that leave the grid through the
 // strip's left / right boundary lane; GENERAL additionally applies the row masks of the first
 // and last two rows of the cloth (uniform per step).
-template <bool ALPHA1, bool GENERAL>
+template <bool ALPHA1, bool GENERAL, bool TAIL>
 __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, const float* row1,
                                           const float* row2, int lane, float mL, float mRt,
                                           float mR, float m1, float m2, float (&A0)[4],
@@ -128,6 +128,36 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   load8(row1 + (3 + d) * BOXW, lane, v1);
   load4(row2 + d * BOXW, lane, x2);
   load4(row2 + (3 + d) * BOXW, lane, v2);
+  if (TAIL) {
+    // rows R >= y1 are not owned: only the pushes into rows R-1, R-2 (a-sides of the edges
+    // that reach up to row R) are still needed
+    float dummy = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      edge<ALPHA1, true, false>(f, 1, 3, x1[k + 2] - xr[k + 2], v1[k + 2] - vr[k + 2], A1[k],
+                                dummy);
+      edge<ALPHA1, true, false>(f, 9, 11, x2[k] - xr[k + 2], v2[k] - vr[k + 2], A0[k], dummy);
+    }
+#pragma unroll
+    for (int e = 1; e < 5; ++e) {
+      float dx = x1[e + 1] - xr[e + 2], dv = v1[e + 1] - vr[e + 2];
+      if (e == 4) {
+        dx *= mRt;
+        dv *= mRt;
+      }
+      edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[e - 1], dummy);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float dx = x1[e + 2] - xr[e + 1], dv = v1[e + 2] - vr[e + 1];
+      if (e == 0) {
+        dx *= mL;
+        dv *= mL;
+      }
+      edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[e], dummy);
+    }
+    return;
+  }
   // init row R: b + v*wV
 #pragma unroll
   for (int k = 0; k < 4; ++k) A2[k] = fmaf(vr[k + 2], f.wv, f.b[d]);
@@ -229,8 +259,10 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   const int ix0 = x0 + FW * lane;
   const int nx = a.nx, ny = a.ny;
 
-  const int r_first = y0 - 2;  // first row entering the window
-  const int r_last = y1 + 1;   // last row entering the window (finishes row y1-1)
+  // Rows y0-2 .. y1+1 pass through the ring; arithmetic starts at row y0 (the two rows below
+  // only feed rows < y0) and the last two steps (rows y1, y1+1) only finish rows y1-2, y1-1.
+  const int r_first = y0 - 2;
+  const int r_last = y1 + 1;
 
   if (lane == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&full[s], 1);
@@ -245,8 +277,11 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   };
   if (lane == 0) {
     issue(r_first);
-    if (r_first + 1 <= r_last) issue(r_first + 1);
+    issue(r_first + 1);
+    issue(r_first + 2);
   }
+  mbar_wait(&full[0], 0);
+  mbar_wait(&full[1], 0);
 
   // nx % 4 == 0 (fast_supported): only a strip's outermost lanes own edges leaving the grid
   const float mL = ix0 >= 1 ? 1.0f : 0.0f;
@@ -267,32 +302,36 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     for (int k = 0; k < 4; ++k) A0[d][k] = A1[d][k] = A2[d][k] = 0.0f;
 
 #pragma unroll 1
-  for (int R = r_first; R <= r_last; ++R) {
+  for (int R = y0; R <= r_last; ++R) {
     const int t = R - r_first;
     __syncwarp();
-    if (lane == 0 && R + 2 <= r_last) {
+    if (lane == 0 && R + 1 <= r_last) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(R + 2);
+      issue(R + 1);
     }
     mbar_wait(&full[t % RING], (t / RING) & 1);
 
     const float* rowR = ring + (t % RING) * ROWF;
     const float* row1 = ring + ((t + RING - 1) % RING) * ROWF;
     const float* row2 = ring + ((t + RING - 2) % RING) * ROWF;
-    if (R - 2 >= 0 && R < ny) {
+    if (R >= y1) {
+      if (R < ny) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          comp_pass<ALPHA1, false, true>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f,
+                                         A0[d], A1[d], A2[d], d);
+      }
+    } else if (R >= 2) {
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        comp_pass<ALPHA1, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f, A0[d], A1[d],
-                                 A2[d], d);
+        comp_pass<ALPHA1, false, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f, A0[d],
+                                        A1[d], A2[d], d);
     } else {
-      const bool okR = R >= 0 && R < ny;
-      const float mR = okR ? 1.f : 0.f;
-      const float m1 = (okR && R - 1 >= 0) ? 1.f : 0.f;
-      const float m2 = (okR && R - 2 >= 0) ? 1.f : 0.f;
+      const float m1 = R >= 1 ? 1.f : 0.f;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        comp_pass<ALPHA1, true>(f, rowR, row1, row2, lane, mL, mRt, mR, m1, m2, A0[d], A1[d],
-                                A2[d], d);
+        comp_pass<ALPHA1, true, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, m1, 0.f, A0[d],
+                                       A1[d], A2[d], d);
     }
 
     // row R-2 is complete: plug, integrate, collide, pin, store
