@@ -124,7 +124,7 @@ struct sc_ctx {
   FastNet fast{};
   bool fast_ok = false;
   FastPlan plan{};
-  CUtensorMap tmap[2];
+  CUtensorMap tmap[2][2];  // [buffer][xy pairs | z planes]
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
   bool health_on = false;  // non-finite tracking in device-resident stepping
@@ -275,6 +275,8 @@ void upload_scene(sc_ctx* c, const sc_scene_desc* s) {
       pln.push_back(pc);
     }
     k.n_pins = d.n_pins;
+    k.pin_row_lo = d.n_pins > 0 ? d.pin_nodes[0] / s->nx : 0;  // pins are sorted
+    k.pin_row_hi = d.n_pins > 0 ? d.pin_nodes[d.n_pins - 1] / s->nx : -1;
     k.pin_word0 = 0;
     k.anchor0 = static_cast<int64_t>(anchors.size() / 3);
     if (d.n_pins > 0) {
@@ -330,20 +332,38 @@ void build_tmaps(sc_ctx* c) {
   if (c->prec != SC_F32) return;
   PFN_encodeTiled enc = get_encoder();
   if (!enc) throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver"};
+  const cuuint64_t S = static_cast<cuuint64_t>(c->plane_stride);
   for (int i = 0; i < 2; ++i) {
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->pitch),
-                                static_cast<cuuint64_t>(c->rows_local),
-                                static_cast<cuuint64_t>(6) * c->batch};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->pitch) * 4,
-                                   static_cast<cuuint64_t>(c->plane_stride) * 4};
-    const cuuint32_t box[3] = {136, 1, 6};  // see fast_kernels.cu (BOXW)
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = enc(&c->tmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->state[i], dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+    // xy pairs as 8-byte elements: dims (pitch, rows, {x,v}, batch)
+    {
+      const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c->pitch),
+                                  static_cast<cuuint64_t>(c->rows_local), 2,
+                                  static_cast<cuuint64_t>(c->batch)};
+      const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c->pitch) * 8, S * 8, S * 24};
+      const cuuint32_t box[4] = {136, 1, 2, 1};  // see fast_kernels.cu (BOXW)
+      const cuuint32_t estr[4] = {1, 1, 1, 1};
+      const CUresult r = enc(&c->tmap[i][0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->state[i],
+                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled(xy) failed (" + std::to_string(r) + ")"};
+    }
+    // z planes: dims (pitch, rows, {x,v}, batch), base at element 4S
+    {
+      const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c->pitch),
+                                  static_cast<cuuint64_t>(c->rows_local), 2,
+                                  static_cast<cuuint64_t>(c->batch)};
+      const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c->pitch) * 4, S * 4, S * 24};
+      const cuuint32_t box[4] = {136, 1, 2, 1};
+      const cuuint32_t estr[4] = {1, 1, 1, 1};
+      const CUresult r = enc(&c->tmap[i][1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                             static_cast<float*>(c->state[i]) + 4 * S, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        throw Fail{SC_ERR_CUDA, "cuTensorMapEncodeTiled(z) failed (" + std::to_string(r) + ")"};
+    }
   }
   c->tmap_ok = true;
 }
@@ -406,7 +426,7 @@ void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, doubl
     if (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok) {
       FastPlan plan = c->plan;
       if (u0 != c->u0 || u1 != c->u1) plan = plan_fast(c->nx, u1 - u0, c->batch, c->device);
-      e = launch_fast(a, c->fast, &c->tmap[c->cur], plan, stream);
+      e = launch_fast(a, c->fast, c->tmap[c->cur], plan, stream);
     } else {
       e = launch_parity<float>(a, kind, stream);
     }
@@ -865,20 +885,25 @@ void halo_copy(sc_ctx* c, int side, void* dev, bool pack, cudaStream_t st) {
   else
     grow = side == 0 ? c->u0 - 2 : c->u1;
   const size_t e = c->elem();
+  const int64_t S = c->plane_stride;
   unsigned char* buf = static_cast<unsigned char*>(c->state[1 - c->cur]);
+  // halo buffer [2 rows][x.xy 2nx | v.xy 2nx | x.z nx | v.z nx] = 6*nx elements per row
   for (int r = 0; r < 2; ++r) {
     const int g = grow + r;
     if (g < 0 || g >= c->ny) continue;
-    const int lr = g - c->g0;
-    for (int p = 0; p < 6; ++p) {
-      unsigned char* dst_state = buf + (static_cast<size_t>(p) * c->plane_stride +
-                                        static_cast<size_t>(lr) * c->pitch) * e;
-      unsigned char* hal = static_cast<unsigned char*>(dev) +
-                           (static_cast<size_t>(p) * 2 + r) * c->nx * e;
+    const int64_t lr = g - c->g0;
+    const int64_t seg_off[4] = {elem_index(0, lr, 0, c->pitch, S), elem_index(3, lr, 0, c->pitch, S),
+                                elem_index(2, lr, 0, c->pitch, S), elem_index(5, lr, 0, c->pitch, S)};
+    const int64_t seg_len[4] = {2LL * c->nx, 2LL * c->nx, c->nx, c->nx};
+    int64_t hoff = static_cast<int64_t>(r) * 6 * c->nx;
+    for (int q = 0; q < 4; ++q) {
+      unsigned char* st_ptr = buf + seg_off[q] * e;
+      unsigned char* h_ptr = static_cast<unsigned char*>(dev) + hoff * e;
       if (pack)
-        ck(cudaMemcpyAsync(hal, dst_state, c->nx * e, cudaMemcpyDeviceToDevice, st), "halo");
+        ck(cudaMemcpyAsync(h_ptr, st_ptr, seg_len[q] * e, cudaMemcpyDeviceToDevice, st), "halo");
       else
-        ck(cudaMemcpyAsync(dst_state, hal, c->nx * e, cudaMemcpyDeviceToDevice, st), "halo");
+        ck(cudaMemcpyAsync(st_ptr, h_ptr, seg_len[q] * e, cudaMemcpyDeviceToDevice, st), "halo");
+      hoff += seg_len[q];
     }
   }
 }

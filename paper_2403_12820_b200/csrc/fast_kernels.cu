@@ -4,10 +4,13 @@
 // Design:
 //  * Warp = one 128-column strip of one cloth, marching upward over a segment of rows. Each lane
 //    owns 4 consecutive columns (float4 in every plane).
-//  * Rows are staged in a 6-slot shared-memory ring by TMA (cp.async.bulk.tensor.3d, one box of
-//    136 columns x 1 row x 6 planes per row starting at the 16-byte-aligned column x0-4 — TMA
-//    rejects unaligned starts — with negative / past-the-end coordinates zero-filled), two rows
-//    ahead of use, so HBM latency hides behind the arithmetic.
+//  * Rows are staged in a 5-slot shared-memory ring by TMA (two cp.async.bulk.tensor.4d boxes per
+//    row: the interleaved (x,y) pairs of x and v as 8-byte elements, and the z planes; 136
+//    columns from the 16-byte-aligned column x0-4 — TMA rejects unaligned starts — with
+//    negative / past-the-end coordinates zero-filled), one row ahead of use.
+//  * x and y components are processed as packed f32x2 pairs (FADD2/FFMA2/FMUL2 with the channel
+//    weights as scalar-broadcast operands), z as plain f32: two instruction streams for three
+//    components.
 //  * Edge sharing: the 12 stencil channels are 6 undirected edge types (E, E2, N, N2, NE, NW).
 //    Each edge's difference, ISRU (one MUFU.RSQ) and derivative product are computed once and
 //    pushed into both endpoint accumulators (isru is odd and differences are antisymmetric, so
@@ -31,8 +34,12 @@ constexpr int FW = 4;              // columns per lane
 constexpr int STRIP = 32 * FW;     // columns per warp
 constexpr int BOXW = STRIP + 8;    // staged columns x0-4 .. x0+131 (2-column halo + alignment)
 constexpr int RING = 5;            // staged rows: R-3 .. R+1 (one row of prefetch)
-constexpr int ROW_BYTES = 6 * BOXW * 4;            // bytes one TMA box delivers (6 planes)
-constexpr int ROWF = ((ROW_BYTES + 127) / 128) * 32;  // ring slot stride in floats (128 B aligned)
+// ring slot (floats): [x.xy: BOXW pairs][v.xy: BOXW pairs][x.z: BOXW][v.z: BOXW]
+constexpr int XY_X = 0, XY_V = 2 * BOXW, Z_X = 4 * BOXW, Z_V = 5 * BOXW;
+constexpr int XY_BYTES = 4 * BOXW * 4;                 // first TMA box
+constexpr int ROW_BYTES = 6 * BOXW * 4;                // both boxes
+constexpr int ROWF = ((ROW_BYTES + 127) / 128) * 32;   // slot stride in floats (128 B aligned)
+static_assert((XY_BYTES % 128) == 0, "z box must start 128-byte aligned");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,12 +67,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_row(float* dst, const CUtensorMap* map, int c0, int c1,
-                                             int c2, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_4d(float* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -76,83 +84,131 @@ __device__ __forceinline__ float rsqrt_q(float q) {
   return r;
 }
 
+// ---- f32 / packed f32x2 arithmetic with scalar-broadcast weights ---------------------------
+__device__ __forceinline__ float vsub(float a, float b) { return a - b; }
+__device__ __forceinline__ float2 vsub(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float vmul(float a, float b) { return a * b; }
+__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float vscale(float a, float m) { return a * m; }
+__device__ __forceinline__ float2 vscale(float2 a, float m) {
+  return __fmul2_rn(a, make_float2(m, m));
+}
+__device__ __forceinline__ float vfma(float a, float w, float c) { return fmaf(a, w, c); }
+__device__ __forceinline__ float2 vfma(float2 a, float w, float2 c) {
+  return __ffma2_rn(a, make_float2(w, w), c);
+}
+__device__ __forceinline__ float vfmav(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ float2 vfmav(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float vsplat(float w) { return w; }
+__device__ __forceinline__ float2 vsplat2(float w) { return make_float2(w, w); }
+__device__ __forceinline__ float vq(float dx) { return fmaf(dx, dx, 1.0f); }
+__device__ __forceinline__ float2 vq(float2 dx) { return __ffma2_rn(dx, dx, make_float2(1.f, 1.f)); }
+__device__ __forceinline__ float vqa(float dx, float al) { return fmaf(dx * al, dx, 1.0f); }
+__device__ __forceinline__ float2 vqa(float2 dx, float al) {
+  return __ffma2_rn(__fmul2_rn(dx, make_float2(al, al)), dx, make_float2(1.f, 1.f));
+}
+__device__ __forceinline__ float vrsq(float q) { return rsqrt_q(q); }
+__device__ __forceinline__ float2 vrsq(float2 q) { return make_float2(rsqrt_q(q.x), rsqrt_q(q.y)); }
+
 // Edge contribution to its origin node a (channel ca) and far node b (channel cb = -ca):
 //   a: acc += dx*wL'_ca + s*(wN'_ca + dv*wD'_ca)
 //   b: acc += dx*(-wL'_cb) + s*(dv*wD'_cb - wN'_cb)
 // with dx = x_a - x_b, dv = v_a - v_b, s = dx * rsqrt(1 + alpha'_c dx^2) and the gains folded
 // into the primed weights (wL' = g wL, wN' = g wN, wD' = g^2 wD, alpha' = alpha g^2).
 // Invalid edges (an endpoint outside the grid) arrive with dx = dv = 0 and contribute exactly 0.
-template <bool ALPHA1, bool PA, bool PB>
-__device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, float dx, float dv,
-                                     float& acc_a, float& acc_b) {
-  const float q = ALPHA1 ? fmaf(dx, dx, 1.0f) : fmaf(dx * f.alpha[ca], dx, 1.0f);
-  const float s = dx * rsqrt_q(q);
+template <bool ALPHA1, bool PA, bool PB, typename V>
+__device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, V dx, V dv, V& acc_a,
+                                     V& acc_b) {
+  const V q = ALPHA1 ? vq(dx) : vqa(dx, f.alpha[ca]);
+  const V s = vmul(dx, vrsq(q));
   if (PA) {
-    const float t = fmaf(dv, f.wd[ca], f.wn[ca]);
-    acc_a = fmaf(dx, f.wl[ca], acc_a);
-    acc_a = fmaf(s, t, acc_a);
+    const V t = vfma(dv, f.wd[ca], [&] {
+      if constexpr (sizeof(V) == 8) return vsplat2(f.wn[ca]); else return vsplat(f.wn[ca]);
+    }());
+    acc_a = vfma(dx, f.wl[ca], acc_a);
+    acc_a = vfmav(s, t, acc_a);
   }
   if (PB) {
-    const float t = fmaf(dv, f.wd[cb], f.nwn[cb]);
-    acc_b = fmaf(dx, f.nwl[cb], acc_b);
-    acc_b = fmaf(s, t, acc_b);
+    const V t = vfma(dv, f.wd[cb], [&] {
+      if constexpr (sizeof(V) == 8) return vsplat2(f.nwn[cb]); else return vsplat(f.nwn[cb]);
+    }());
+    acc_b = vfma(dx, f.nwl[cb], acc_b);
+    acc_b = vfmav(s, t, acc_b);
   }
 }
 
-// Lane window of a staged row: columns ix0-2 .. ix0+5 <-> box index 4*lane+2 .. 4*lane+9.
-__device__ __forceinline__ void load8(const float* base, int lane, float* o) {
-  const float2 l = *reinterpret_cast<const float2*>(base + FW * lane + 2);
-  const float4 m = *reinterpret_cast<const float4*>(base + FW * lane + 4);
-  const float2 r = *reinterpret_cast<const float2*>(base + FW * lane + 8);
+// Lane windows of a staged row: columns ix0-2 .. ix0+5 <-> box column 4*lane+2 .. 4*lane+9,
+// columns ix0 .. ix0+3 <-> 4*lane+4 .. 4*lane+7.
+__device__ __forceinline__ void win8(const float* zplane, int lane, float* o) {
+  const float2 l = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
+  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+  const float2 r = *reinterpret_cast<const float2*>(zplane + FW * lane + 8);
   o[0] = l.x; o[1] = l.y; o[2] = m.x; o[3] = m.y; o[4] = m.z; o[5] = m.w; o[6] = r.x; o[7] = r.y;
 }
-
-__device__ __forceinline__ void load4(const float* base, int lane, float* o) {
-  const float4 m = *reinterpret_cast<const float4*>(base + FW * lane + 4);
+__device__ __forceinline__ void win8(const float* xyplane, int lane, float2* o) {
+  const float4* p = reinterpret_cast<const float4*>(xyplane + 2 * (FW * lane + 2));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 m = p[q];
+    o[2 * q] = make_float2(m.x, m.y);
+    o[2 * q + 1] = make_float2(m.z, m.w);
+  }
+}
+__device__ __forceinline__ void win4(const float* zplane, int lane, float* o) {
+  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
   o[0] = m.x; o[1] = m.y; o[2] = m.z; o[3] = m.w;
 }
+__device__ __forceinline__ void win4(const float* xyplane, int lane, float2* o) {
+  const float4* p = reinterpret_cast<const float4*>(xyplane + 2 * (FW * lane + 4));
+  const float4 a = p[0], b = p[1];
+  o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w);
+  o[2] = make_float2(b.x, b.y); o[3] = make_float2(b.z, b.w);
+}
 
-// All edges of one component whose upper endpoint lies on row R, pushed into the accumulators
-// of rows R-2 (A0), R-1 (A1), R (A2). mL / mRt zero the edges that leave the grid through the
-// strip's left / right boundary lane; GENERAL additionally applies the row masks of the first
-// and last two rows of the cloth (uniform per step).
-template <bool ALPHA1, bool GENERAL, bool TAIL>
-__device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, const float* row1,
-                                          const float* row2, int lane, float mL, float mRt,
-                                          float mR, float m1, float m2, float (&A0)[4],
-                                          float (&A1)[4], float (&A2)[4], int d) {
-  float xr[8], vr[8], x1[8], v1[8], x2[4], v2[4];
-  load8(rowR + d * BOXW, lane, xr);
-  load8(rowR + (3 + d) * BOXW, lane, vr);
-  load8(row1 + d * BOXW, lane, x1);
-  load8(row1 + (3 + d) * BOXW, lane, v1);
-  load4(row2 + d * BOXW, lane, x2);
-  load4(row2 + (3 + d) * BOXW, lane, v2);
+// All edges of one component group (V = float2: x,y packed; V = float: z) whose upper
+// endpoint lies on row R, pushed into the accumulators of rows R-2 (A0), R-1 (A1), R (A2).
+// mL / mRt zero the edges that leave the grid through a strip's boundary lane; GENERAL applies
+// the row masks of the first two rows of the cloth; TAIL (rows R >= y1, not owned) keeps only
+// the pushes into rows R-1 and R-2.
+template <bool ALPHA1, bool GENERAL, bool TAIL, typename V>
+__device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, const float* vR,
+                                          const float* x1p, const float* v1p, const float* x2p,
+                                          const float* v2p, int lane, float mL, float mRt,
+                                          float m1, float m2, V (&A0)[4], V (&A1)[4], V (&A2)[4],
+                                          V bias) {
+  V xr[8], vr[8], x1[8], v1[8], x2[4], v2[4];
+  win8(xR, lane, xr);
+  win8(vR, lane, vr);
+  win8(x1p, lane, x1);
+  win8(v1p, lane, v1);
+  win4(x2p, lane, x2);
+  win4(v2p, lane, v2);
+  V dummy{};
   if (TAIL) {
-    // rows R >= y1 are not owned: only the pushes into rows R-1, R-2 (a-sides of the edges
-    // that reach up to row R) are still needed
-    float dummy = 0.0f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      edge<ALPHA1, true, false>(f, 1, 3, x1[k + 2] - xr[k + 2], v1[k + 2] - vr[k + 2], A1[k],
+      edge<ALPHA1, true, false>(f, 1, 3, vsub(x1[k + 2], xr[k + 2]), vsub(v1[k + 2], vr[k + 2]),
+                                A1[k], dummy);
+      edge<ALPHA1, true, false>(f, 9, 11, vsub(x2[k], xr[k + 2]), vsub(v2[k], vr[k + 2]), A0[k],
                                 dummy);
-      edge<ALPHA1, true, false>(f, 9, 11, x2[k] - xr[k + 2], v2[k] - vr[k + 2], A0[k], dummy);
     }
 #pragma unroll
     for (int e = 1; e < 5; ++e) {
-      float dx = x1[e + 1] - xr[e + 2], dv = v1[e + 1] - vr[e + 2];
+      V dx = vsub(x1[e + 1], xr[e + 2]), dv = vsub(v1[e + 1], vr[e + 2]);
       if (e == 4) {
-        dx *= mRt;
-        dv *= mRt;
+        dx = vscale(dx, mRt);
+        dv = vscale(dv, mRt);
       }
       edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[e - 1], dummy);
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float dx = x1[e + 2] - xr[e + 1], dv = v1[e + 2] - vr[e + 1];
+      V dx = vsub(x1[e + 2], xr[e + 1]), dv = vsub(v1[e + 2], vr[e + 1]);
       if (e == 0) {
-        dx *= mL;
-        dv *= mL;
+        dx = vscale(dx, mL);
+        dv = vscale(dv, mL);
       }
       edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[e], dummy);
     }
@@ -160,22 +216,16 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   }
   // init row R: b + v*wV
 #pragma unroll
-  for (int k = 0; k < 4; ++k) A2[k] = fmaf(vr[k + 2], f.wv, f.b[d]);
+  for (int k = 0; k < 4; ++k) A2[k] = vfma(vr[k + 2], f.wv, bias);
 
-  float dummy = 0.0f;
-  auto mask_of = [&](int e, int lo, int hi, float row) -> float {
-    // lane-column mask for slot e of an edge family whose slots < lo / > hi may leave the grid
-    float m = e < lo ? mL : (e > hi ? mRt : 1.0f);
-    return GENERAL ? m * row : m;
-  };
   // E edges in row R: a = col ix0-1+e (j = e+1), b = col ix0+e (j = e+2)
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
-    float dx = xr[e + 1] - xr[e + 2], dv = vr[e + 1] - vr[e + 2];
-    if (GENERAL || e == 0 || e == 4) {
-      const float m = mask_of(e, 1, 3, mR);
-      dx *= m;
-      dv *= m;
+    V dx = vsub(xr[e + 1], xr[e + 2]), dv = vsub(vr[e + 1], vr[e + 2]);
+    if (e == 0 || e == 4) {
+      const float m = e == 0 ? mL : mRt;
+      dx = vscale(dx, m);
+      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, A2[3], dummy);
@@ -184,11 +234,11 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   // E2 edges in row R: a = col ix0-2+e (j = e), b = col ix0+e (j = e+2)
 #pragma unroll
   for (int e = 0; e < 6; ++e) {
-    float dx = xr[e] - xr[e + 2], dv = vr[e] - vr[e + 2];
-    if (GENERAL || e <= 1 || e >= 4) {
-      const float m = mask_of(e, 2, 3, mR);
-      dx *= m;
-      dv *= m;
+    V dx = vsub(xr[e], xr[e + 2]), dv = vsub(vr[e], vr[e + 2]);
+    if (e <= 1 || e >= 4) {
+      const float m = e <= 1 ? mL : mRt;
+      dx = vscale(dx, m);
+      dv = vscale(dv, m);
     }
     if (e <= 1) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy, A2[e]);
     else if (e >= 4) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[e - 2], dummy);
@@ -197,27 +247,27 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   // N edges (R-1 -> R) and N2 edges (R-2 -> R), owned columns
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    float dx = x1[k + 2] - xr[k + 2], dv = v1[k + 2] - vr[k + 2];
+    V dx = vsub(x1[k + 2], xr[k + 2]), dv = vsub(v1[k + 2], vr[k + 2]);
     if (GENERAL) {
-      dx *= m1;
-      dv *= m1;
+      dx = vscale(dx, m1);
+      dv = vscale(dv, m1);
     }
     edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[k], A2[k]);
-    float dx2 = x2[k] - xr[k + 2], dv2 = v2[k] - vr[k + 2];
+    V dx2 = vsub(x2[k], xr[k + 2]), dv2 = vsub(v2[k], vr[k + 2]);
     if (GENERAL) {
-      dx2 *= m2;
-      dv2 *= m2;
+      dx2 = vscale(dx2, m2);
+      dv2 = vscale(dv2, m2);
     }
     edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[k], A2[k]);
   }
   // NE edges: a = (ix0-1+e, R-1) (j = e+1), b = (ix0+e, R) (j = e+2)
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
-    float dx = x1[e + 1] - xr[e + 2], dv = v1[e + 1] - vr[e + 2];
+    V dx = vsub(x1[e + 1], xr[e + 2]), dv = vsub(v1[e + 1], vr[e + 2]);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = mask_of(e, 1, 3, m1);
-      dx *= m;
-      dv *= m;
+      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
+      dx = vscale(dx, m);
+      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[3], dummy);
@@ -226,11 +276,11 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   // NW edges: a = (ix0+e, R-1) (j = e+2), b = (ix0+e-1, R) (j = e+1)
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
-    float dx = x1[e + 2] - xr[e + 1], dv = v1[e + 2] - vr[e + 1];
+    V dx = vsub(x1[e + 2], xr[e + 1]), dv = vsub(v1[e + 2], vr[e + 1]);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = mask_of(e, 1, 3, m1);
-      dx *= m;
-      dv *= m;
+      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
+      dx = vscale(dx, m);
+      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[0], dummy);
     else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, A2[3]);
@@ -238,12 +288,32 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* rowR, c
   }
 }
 
+template <bool ALPHA1, bool GENERAL, bool TAIL>
+__device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, const float* row1,
+                                         const float* row2, int lane, float mL, float mRt,
+                                         float m1, float m2, float2 (&P0)[4], float2 (&P1)[4],
+                                         float2 (&P2)[4], float (&Z0)[4], float (&Z1)[4],
+                                         float (&Z2)[4]) {
+  comp_pass<ALPHA1, GENERAL, TAIL, float2>(f, rowR + XY_X, rowR + XY_V, row1 + XY_X, row1 + XY_V,
+                                           row2 + XY_X, row2 + XY_V, lane, mL, mRt, m1, m2, P0,
+                                           P1, P2, make_float2(f.b[0], f.b[1]));
+  comp_pass<ALPHA1, GENERAL, TAIL, float>(f, rowR + Z_X, rowR + Z_V, row1 + Z_X, row1 + Z_V,
+                                          row2 + Z_X, row2 + Z_V, lane, mL, mRt, m1, m2, Z0, Z1,
+                                          Z2, f.b[2]);
+}
+
+// component d of x (X = true) or v at box column j of a ring slot
+__device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int j) {
+  return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * j + d] : slot[(X ? Z_X : Z_V) + j];
+}
+
 template <bool ALPHA1>
-__global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
+                                                      const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
                                                       const int n_segs) {
-  extern __shared__ __align__(128) float ring[];  // [RING][6][BOXW] (slot stride ROWF)
+  extern __shared__ __align__(128) float ring[];  // [RING][ROWF]
   __shared__ __align__(8) uint64_t full[RING];
   __shared__ float scratch[32][13];  // per-lane impulse staging for the collider finish
 
@@ -272,8 +342,10 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   auto issue = [&](int row) {  // lane 0 only
     const int t = row - r_first;
     uint64_t* bar = &full[t % RING];
+    float* slot = ring + (t % RING) * ROWF;
     mbar_expect_tx(bar, ROW_BYTES);
-    tma_load_row(ring + (t % RING) * ROWF, &tmap, x0 - 4, row - a.g0, 6 * b, bar);
+    tma_load_4d(slot, &tmap_xy, x0 - 4, row - a.g0, 0, b, bar);
+    tma_load_4d(slot + Z_X, &tmap_z, x0 - 4, row - a.g0, 0, b, bar);
   };
   if (lane == 0) {
     issue(r_first);
@@ -292,14 +364,18 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
-  float* out_b = a.out + static_cast<int64_t>(b) * 6 * a.plane_stride;
+  const int64_t S = a.plane_stride;
+  float* out_b = a.out + static_cast<int64_t>(b) * 6 * S;
   const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
 
-  float A0[3][4], A1[3][4], A2[3][4];  // [component][column] for rows R-2, R-1, R
+  // accumulators [column] for rows R-2 (P0/Z0), R-1 (P1/Z1), R (P2/Z2): P = (x,y), Z = z
+  float2 P0[4], P1[4], P2[4];
+  float Z0[4], Z1[4], Z2[4];
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) A0[d][k] = A1[d][k] = A2[d][k] = 0.0f;
+  for (int k = 0; k < 4; ++k) {
+    P0[k] = P1[k] = P2[k] = make_float2(0.f, 0.f);
+    Z0[k] = Z1[k] = Z2[k] = 0.f;
+  }
 
 #pragma unroll 1
   for (int R = y0; R <= r_last; ++R) {
@@ -315,50 +391,46 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     const float* row1 = ring + ((t + RING - 1) % RING) * ROWF;
     const float* row2 = ring + ((t + RING - 2) % RING) * ROWF;
     if (R >= y1) {
-      if (R < ny) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-          comp_pass<ALPHA1, false, true>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f,
-                                         A0[d], A1[d], A2[d], d);
-      }
+      if (R < ny)
+        row_pass<ALPHA1, false, true>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2,
+                                      Z0, Z1, Z2);
     } else if (R >= 2) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        comp_pass<ALPHA1, false, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, 1.f, A0[d],
-                                        A1[d], A2[d], d);
+      row_pass<ALPHA1, false, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2, Z0,
+                                     Z1, Z2);
     } else {
-      const float m1 = R >= 1 ? 1.f : 0.f;
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        comp_pass<ALPHA1, true, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, m1, 0.f, A0[d],
-                                       A1[d], A2[d], d);
+      row_pass<ALPHA1, true, false>(f, rowR, row1, row2, lane, mL, mRt, R >= 1 ? 1.f : 0.f, 0.f,
+                                    P0, P1, P2, Z0, Z1, Z2);
     }
 
     // row R-2 is complete: plug, integrate, collide, pin, store
     const int Rf = R - 2;
     if (Rf >= y0 && Rf < y1 && lane_live) {
-      float xs[3][4], vs[3][4];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        load4(row2 + d * BOXW, lane, xs[d]);
-        load4(row2 + (3 + d) * BOXW, lane, vs[d]);
-      }
-      float xo[3][4], vo[3][4];
+      const int64_t lr = Rf - a.g0;
       if (simple) {
+        float2 xs[4], vs[4];
+        float xz[4], vz[4];
+        win4(row2 + XY_X, lane, xs);
+        win4(row2 + XY_V, lane, vs);
+        win4(row2 + Z_X, lane, xz);
+        win4(row2 + Z_V, lane, vz);
         // add_plug_impulse gravity/drag + advance without colliders, IEEE-exact like PARITY
+        float xo[3][4], vo[3][4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          const float xin[3] = {xs[k].x, xs[k].y, xz[k]};
+          const float vin[3] = {vs[k].x, vs[k].y, vz[k]};
+          const float acc[3] = {P0[k].x, P0[k].y, Z0[k]};
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            float imp = A0[d][k];
+            float imp = acc[d];
             if (cc.plug_gravity) imp = __fadd_rn(imp, cc.dv[d]);
-            if (cc.plug_drag) imp = __fsub_rn(imp, __fmul_rn(vs[d][k], cc.drag_c));
-            const float vv = __fadd_rn(vs[d][k], imp);
+            if (cc.plug_drag) imp = __fsub_rn(imp, __fmul_rn(vin[d], cc.drag_c));
+            const float vv = __fadd_rn(vin[d], imp);
             vo[d][k] = vv;
-            xo[d][k] = __fadd_rn(xs[d][k], __fmul_rn(vv, cc.dt));
+            xo[d][k] = __fadd_rn(xin[d], __fmul_rn(vv, cc.dt));
           }
         }
-        if (cc.n_pins > 0) {
+        if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int64_t gnode = static_cast<int64_t>(Rf) * nx + ix0 + k;
@@ -379,15 +451,14 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
         if (a.health) {
           bool fin_imp = true, fin = true;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < 4; ++k) {
+            fin_imp = fin_imp && isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(Z0[k]);
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              fin_imp = fin_imp && isfinite(A0[d][k]);
-              fin = fin && isfinite(xo[d][k]) && isfinite(vo[d][k]);
-            }
+            for (int d = 0; d < 3; ++d) fin = fin && isfinite(xo[d][k]) && isfinite(vo[d][k]);
+          }
           if (!fin_imp) {
             for (int k = 0; k < 4; ++k)
-              if (!(isfinite(A0[0][k]) && isfinite(A0[1][k]) && isfinite(A0[2][k]))) {
+              if (!(isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(Z0[k]))) {
                 const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
                                                static_cast<unsigned long long>(Rf * nx + ix0 + k);
                 atomicMin(&a.health[b].impulse_key, key);
@@ -396,22 +467,25 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
           }
           if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
         }
-        float* o = out_b + static_cast<int64_t>(Rf - a.g0) * a.pitch + ix0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          *reinterpret_cast<float4*>(o + d * a.plane_stride) =
-              make_float4(xo[d][0], xo[d][1], xo[d][2], xo[d][3]);
-          *reinterpret_cast<float4*>(o + (3 + d) * a.plane_stride) =
-              make_float4(vo[d][0], vo[d][1], vo[d][2], vo[d][3]);
-        }
+        float* oxy = out_b + 2 * (lr * a.pitch + ix0);
+        float* ovxy = out_b + 2 * S + 2 * (lr * a.pitch + ix0);
+        reinterpret_cast<float4*>(oxy)[0] = make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
+        reinterpret_cast<float4*>(oxy)[1] = make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
+        reinterpret_cast<float4*>(ovxy)[0] = make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
+        reinterpret_cast<float4*>(ovxy)[1] = make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
+        *reinterpret_cast<float4*>(out_b + 4 * S + lr * a.pitch + ix0) =
+            make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
+        *reinterpret_cast<float4*>(out_b + 5 * S + lr * a.pitch + ix0) =
+            make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
       } else {
         // colliders / pressure / mask: one node at a time (compact code, same IEEE-exact chain)
         const float* rs = ring + ((t + RING - 3) % RING) * ROWF;  // row Rf-1
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) scratch[lane][d * 4 + k] = A0[d][k];  // own row only
-        float* o = out_b + static_cast<int64_t>(Rf - a.g0) * a.pitch;
+        for (int k = 0; k < 4; ++k) {
+          scratch[lane][k] = P0[k].x;  // own row of the scratch only: no cross-lane sync
+          scratch[lane][4 + k] = P0[k].y;
+          scratch[lane][8 + k] = Z0[k];
+        }
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
           const int ix = ix0 + k;
@@ -420,9 +494,9 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
           float px[3], pv[3], imp[3], po[3], qo[3];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            px[d] = row2[d * BOXW + j];
-            pv[d] = row2[(3 + d) * BOXW + j];
-            imp[d] = scratch[lane][d * 4 + k];
+            px[d] = slot_val(row2, true, d, j);
+            pv[d] = slot_val(row2, false, d, j);
+            imp[d] = scratch[lane][4 * d + k];
           }
           if (a.health && !(isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]))) {
             const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
@@ -434,20 +508,20 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
             float e[3], n[3], w[3], sv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              e[d] = __fsub_rn(px[d], row2[d * BOXW + j + 1]);
-              n[d] = __fsub_rn(px[d], row1[d * BOXW + j]);
-              w[d] = __fsub_rn(px[d], row2[d * BOXW + j - 1]);
-              sv[d] = __fsub_rn(px[d], rs[d * BOXW + j]);
+              e[d] = __fsub_rn(px[d], slot_val(row2, true, d, j + 1));
+              n[d] = __fsub_rn(px[d], slot_val(row1, true, d, j));
+              w[d] = __fsub_rn(px[d], slot_val(row2, true, d, j - 1));
+              sv[d] = __fsub_rn(px[d], slot_val(rs, true, d, j));
             }
             pressure_plug(cc, interior, e, n, w, sv, imp);
           }
           plug_tail(cc, pv, imp);
           uint8_t mk;
-          advance_node(a, cc, gnode, px, pv, imp, po, qo, mk);
+          advance_node(a, cc, Rf, gnode, px, pv, imp, po, qo, mk);
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            o[d * a.plane_stride + ix] = po[d];
-            o[(3 + d) * a.plane_stride + ix] = qo[d];
+            out_b[elem_index(d, lr, ix, a.pitch, S)] = po[d];
+            out_b[elem_index(3 + d, lr, ix, a.pitch, S)] = qo[d];
           }
           if (a.constrained) a.constrained[b * nodes + gnode] = mk;
           if (a.health && !(isfinite(po[0]) && isfinite(po[1]) && isfinite(po[2]) &&
@@ -458,12 +532,12 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     }
     // rotate accumulator rows
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        A0[d][k] = A1[d][k];
-        A1[d][k] = A2[d][k];
-      }
+    for (int k = 0; k < 4; ++k) {
+      P0[k] = P1[k];
+      P1[k] = P2[k];
+      Z0[k] = Z1[k];
+      Z1[k] = Z2[k];
+    }
   }
 }
 
@@ -544,10 +618,10 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   if (rows <= 0 || a.batch <= 0) return cudaSuccess;
   if (f.alpha1)
     fast_step_kernel<true><<<static_cast<unsigned>(p.units), 32, p.smem, stream>>>(
-        *tmap, a, f, p.n_strips, p.seg_rows, p.n_segs);
+        tmap[0], tmap[1], a, f, p.n_strips, p.seg_rows, p.n_segs);
   else
     fast_step_kernel<false><<<static_cast<unsigned>(p.units), 32, p.smem, stream>>>(
-        *tmap, a, f, p.n_strips, p.seg_rows, p.n_segs);
+        tmap[0], tmap[1], a, f, p.n_strips, p.seg_rows, p.n_segs);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
 // Layout conversion at the C-ABI edge: the reference's AoS VecT<T>[node] (vec3.hpp:9-59)
-// <-> the planar SoA device layout of the step kernels (sc_device.cuh). Only the API edges
+// <-> the xy-interleaved SoA device layout of the step kernels (sc_device.cuh). Only the API edges
 // run these; device-resident stepping never converts.
 #include "sc_kernels.h"
 
@@ -17,11 +17,11 @@ __global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, 
     const int64_t node = i - b * per;
     const int64_t r = node / nx;
     const int64_t c = node - r * nx;
-    T* o = out + b * 6 * plane_stride + r * pitch + c;
+    T* o = out + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      o[d * plane_stride] = x[3 * i + d];
-      o[(3 + d) * plane_stride] = v[3 * i + d];
+      o[elem_index(d, r, c, pitch, plane_stride)] = x[3 * i + d];
+      o[elem_index(3 + d, r, c, pitch, plane_stride)] = v[3 * i + d];
     }
   }
 }
@@ -37,11 +37,11 @@ __global__ void planar_to_aos(const T* __restrict__ in, T* __restrict__ x, T* __
     const int64_t node = i - b * per;
     const int64_t r = node / nx;
     const int64_t c = node - r * nx;
-    const T* s = in + b * 6 * plane_stride + r * pitch + c;
+    const T* s = in + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      if (x) x[3 * i + d] = s[d * plane_stride];
-      if (v) v[3 * i + d] = s[(3 + d) * plane_stride];
+      if (x) x[3 * i + d] = s[elem_index(d, r, c, pitch, plane_stride)];
+      if (v) v[3 * i + d] = s[elem_index(3 + d, r, c, pitch, plane_stride)];
     }
   }
 }

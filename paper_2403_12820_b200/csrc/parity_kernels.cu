@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
       const int lr = gy0 - 2 + ly - a.g0;
       T val = T(0);
       if (gx >= 0 && gx < a.nx && lr >= 0 && lr < rows_local)
-        val = in[p * a.plane_stride + static_cast<int64_t>(lr) * a.pitch + gx];
+        val = in[elem_index(p, lr, gx, a.pitch, a.plane_stride)];
       sm[e] = val;
     }
     __syncthreads();
@@ -133,13 +133,13 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
 
     T xo[3], vo[3];
     uint8_t mask;
-    advance_node(a, cc, gnode, x, v, imp, xo, vo, mask);
-    T* out = a.out + static_cast<int64_t>(b) * 6 * a.plane_stride +
-             static_cast<int64_t>(iy - a.g0) * a.pitch + ix;
+    advance_node(a, cc, iy, gnode, x, v, imp, xo, vo, mask);
+    T* out = a.out + static_cast<int64_t>(b) * 6 * a.plane_stride;
+    const int64_t lr = iy - a.g0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      out[d * a.plane_stride] = xo[d];
-      out[(3 + d) * a.plane_stride] = vo[d];
+      out[elem_index(d, lr, ix, a.pitch, a.plane_stride)] = xo[d];
+      out[elem_index(3 + d, lr, ix, a.pitch, a.plane_stride)] = vo[d];
     }
     if (a.constrained) a.constrained[static_cast<int64_t>(b) * nodes + gnode] = mask;
     if (a.health && !(R::finite(xo[0]) && R::finite(xo[1]) && R::finite(xo[2]) &&

@@ -1,11 +1,12 @@
 // Device-side definitions shared by the PARITY and FAST step kernels.
 //
-// HBM layout: one ctx holds `batch` cloths; cloth b's state is 6 planar fields
-//   plane p in {x.x, x.y, x.z, v.x, v.y, v.z}, row r (local), column c:
-//   state[(b*6 + p) * plane_stride + r * pitch + c],   plane_stride = rows_local * pitch
-// with pitch = nx rounded up to 4 (16-byte rows for float4/TMA). Validity masks, pins and
-// collider constants are computed from (ix, iy) or read from small per-cloth tables, so a step
-// moves exactly 48 B per node (f32): x and v read once and written once.
+// HBM layout: one ctx holds `batch` cloths; cloth b owns a block of 6*S elements
+// (S = plane_stride = rows_local * pitch, pitch = nx rounded up to 4) holding, row-major,
+//   [x.xy: S interleaved (x,y) pairs][v.xy: S pairs][x.z: S][v.z: S]
+// i.e. the x/y components of a node sit next to each other (one 8-byte element) so the FAST
+// kernel processes them as packed f32x2 pairs, while z is a plain plane. Validity masks, pins
+// and collider constants come from (ix, iy) or small per-cloth tables, so a step moves exactly
+// 48 B per node (f32): x and v read once and written once.
 #pragma once
 
 #include <cstdint>
@@ -23,6 +24,21 @@ __host__ __device__ constexpr int off_dx(int c) {
 __host__ __device__ constexpr int off_dy(int c) {
   return c == 0 ? 0 : c == 1 ? 1 : c == 2 ? 0 : c == 3 ? -1 : c == 4 ? 1 : c == 5 ? 1
        : c == 6 ? -1 : c == 7 ? -1 : c == 8 ? 0 : c == 9 ? 2 : c == 10 ? 0 : -2;
+}
+
+// Element index of component p (0..5 = x.x x.y x.z v.x v.y v.z) of local row r, column c
+// within one cloth's block (see the layout above).
+__host__ __device__ __forceinline__ int64_t elem_index(int p, int64_t r, int64_t c, int64_t pitch,
+                                                       int64_t S) {
+  const int64_t rc = r * pitch + c;
+  switch (p) {
+    case 0: return 2 * rc;
+    case 1: return 2 * rc + 1;
+    case 2: return 4 * S + rc;
+    case 3: return 2 * S + 2 * rc;
+    case 4: return 2 * S + 2 * rc + 1;
+    default: return 5 * S + rc;
+  }
 }
 
 // IEEE round-to-nearest primitives that can never be contracted into FMA. The parity kernels
@@ -72,6 +88,7 @@ struct ClothConst {
   int32_t plug_gravity, plug_drag;
   int32_t n_spheres, sphere0, n_planes, plane0;
   int32_t n_pins;
+  int32_t pin_row_lo, pin_row_hi;  // rows holding pins (skip the bitmap lookup elsewhere)
   int64_t pin_word0;  // first word of this cloth's pin bitmap / rank prefix
   int64_t anchor0;    // first anchor (x3) of this cloth
 };
@@ -143,7 +160,7 @@ __device__ __forceinline__ void plug_tail(const ClothConst<T>& cc, const T v[3],
 
 template <typename T>
 __device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothConst<T>& cc,
-                                             int64_t gnode, const T x[3], const T v[3],
+                                             int row, int64_t gnode, const T x[3], const T v[3],
                                              const T imp[3], T xo[3], T vo[3], uint8_t& mask) {
   using R = RN<T>;
   mask = 0;
@@ -220,7 +237,7 @@ __device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothCo
     }
   }
   // Dirichlet re-pin last (kernels.hpp:245-251): bitmap + rank prefix -> anchor slot
-  if (cc.n_pins > 0) {
+  if (cc.n_pins > 0 && row >= cc.pin_row_lo && row <= cc.pin_row_hi) {
     const int64_t w = cc.pin_word0 + (gnode >> 5);
     const uint32_t bits = __ldg(a.pin_bits + w);
     const uint32_t bit = 1u << (gnode & 31);

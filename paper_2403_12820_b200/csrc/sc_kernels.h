@@ -35,7 +35,8 @@ FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
 bool fast_supported(const NetConst<float>& net, int nx);
 FastPlan plan_fast(int nx, int rows, int batch, int device);
-// tmap: 3-D tensor map over a.in, dims (pitch, local rows, 6*batch), box (136, 1, 6).
+// tmap[0]: xy pairs of a.in as 8-byte elements, dims (pitch, rows, 2, batch), box (136,1,2,1);
+// tmap[1]: z planes, dims (pitch, rows, 2, batch) from element 4S, box (136,1,2,1).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
                         const FastPlan& plan, cudaStream_t stream);
 
