@@ -123,7 +123,9 @@ struct sc_ctx {
   NetConst<double> net64{};
   FastNet fast{};
   bool fast_ok = false;
-  FastPlan plan{};
+  FastPlan plan{};       // simple finish (no colliders / pressure / mask)
+  FastPlan plan_gen{};   // general finish
+  bool any_pressure = false, any_general = false;
   CUtensorMap tmap[2][2];  // [buffer][xy pairs | z planes]
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
@@ -424,8 +426,10 @@ void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, doubl
   cudaError_t e;
   if constexpr (std::is_same<T, float>::value) {
     if (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok) {
-      FastPlan plan = c->plan;
-      if (u0 != c->u0 || u1 != c->u1) plan = plan_fast(c->nx, u1 - u0, c->batch, c->device);
+      FastPlan plan = mask ? c->plan_gen : c->plan;
+      if (u0 != c->u0 || u1 != c->u1)
+        plan = plan_fast(c->nx, u1 - u0, c->batch, c->device, c->any_pressure,
+                         c->any_general || mask != nullptr);
       e = launch_fast(a, c->fast, c->tmap[c->cur], plan, stream);
     } else {
       e = launch_parity<float>(a, kind, stream);
@@ -607,9 +611,18 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       upload_scene<double>(c, s);
     c->health.ensure(static_cast<size_t>(c->batch));
     reset_health(c);
+    c->any_pressure = c->any_general = false;
+    for (int b = 0; b < s->batch; ++b) {
+      const sc_cloth_desc& d = s->cloths[b];
+      const bool pres = d.plug_pressure && static_cast<float>(d.pressure) != 0.0f;
+      c->any_pressure = c->any_pressure || pres;
+      c->any_general = c->any_general || pres || d.n_spheres > 0 || d.n_planes > 0;
+    }
     if (c->prec == SC_F32) {
       build_tmaps(c);
-      c->plan = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device);
+      c->plan = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure,
+                          c->any_general);
+      c->plan_gen = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure, true);
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
     c->has_scene = true;

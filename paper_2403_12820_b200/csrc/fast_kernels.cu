@@ -33,7 +33,8 @@ namespace {
 constexpr int FW = 4;              // columns per lane
 constexpr int STRIP = 32 * FW;     // columns per warp
 constexpr int BOXW = STRIP + 8;    // staged columns x0-4 .. x0+131 (2-column halo + alignment)
-constexpr int RING = 5;            // staged rows: R-3 .. R+1 (one row of prefetch)
+// staged rows: R-3 .. R+1 (RING = 5, when some cloth plugs pressure, whose finish reads row
+// R-3) or R-2 .. R+1 (RING = 4); one row of prefetch
 // ring slot (floats): [x.xy: BOXW pairs][v.xy: BOXW pairs][x.z: BOXW][v.z: BOXW]
 constexpr int XY_X = 0, XY_V = 2 * BOXW, Z_X = 4 * BOXW, Z_V = 5 * BOXW;
 constexpr int XY_BYTES = 4 * BOXW * 4;                 // first TMA box
@@ -307,15 +308,17 @@ __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int 
   return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * j + d] : slot[(X ? Z_X : Z_V) + j];
 }
 
-template <bool ALPHA1>
+template <bool ALPHA1, int RING>
 __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
                                                       const int n_segs) {
-  extern __shared__ __align__(128) float ring[];  // [RING][ROWF]
+  // dynamic smem: [RING][ROWF] ring, then (only when some cloth needs the collider / pressure /
+  // mask finish) a [32][13] per-lane impulse scratch
+  extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[RING];
-  __shared__ float scratch[32][13];  // per-lane impulse staging for the collider finish
+  float (*scratch)[13] = reinterpret_cast<float (*)[13]>(ring + RING * ROWF);
 
   const int lane = threadIdx.x;
   const int unit = blockIdx.x;
@@ -347,6 +350,9 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
     tma_load_4d(slot, &tmap_xy, x0 - 4, row - a.g0, 0, b, bar);
     tma_load_4d(slot + Z_X, &tmap_z, x0 - 4, row - a.g0, 0, b, bar);
   };
+  // programmatic dependent launch: everything above overlapped the previous step's tail; the
+  // state it wrote is read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lane == 0) {
     issue(r_first);
     issue(r_first + 1);
@@ -367,6 +373,9 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   const int64_t S = a.plane_stride;
   float* out_b = a.out + static_cast<int64_t>(b) * 6 * S;
   const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
+  const float dv_eff[3] = {cc.plug_gravity ? cc.dv[0] : 0.f, cc.plug_gravity ? cc.dv[1] : 0.f,
+                           cc.plug_gravity ? cc.dv[2] : 0.f};
+  const float drag_eff = cc.plug_drag ? cc.drag_c : 0.f;
 
   // accumulators [column] for rows R-2 (P0/Z0), R-1 (P1/Z1), R (P2/Z2): P = (x,y), Z = z
   float2 P0[4], P1[4], P2[4];
@@ -422,9 +431,10 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
           const float acc[3] = {P0[k].x, P0[k].y, Z0[k]};
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            float imp = acc[d];
-            if (cc.plug_gravity) imp = __fadd_rn(imp, cc.dv[d]);
-            if (cc.plug_drag) imp = __fsub_rn(imp, __fmul_rn(vin[d], cc.drag_c));
+            // unplugged gravity / drag enter as +0 terms (branch-free; only the sign of an
+            // exactly-zero impulse can differ from skipping them)
+            float imp = __fadd_rn(acc[d], dv_eff[d]);
+            imp = __fsub_rn(imp, __fmul_rn(vin[d], drag_eff));
             const float vv = __fadd_rn(vin[d], imp);
             vo[d][k] = vv;
             xo[d][k] = __fadd_rn(xin[d], __fmul_rn(vv, cc.dt));
@@ -539,6 +549,9 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
       Z1[k] = Z2[k];
     }
   }
+  // let the next step's grid launch once every CTA of this one is done with its work (an early
+  // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 }  // namespace
@@ -570,24 +583,36 @@ bool fast_supported(const NetConst<float>& net, int nx) {
   return true;
 }
 
-size_t fast_smem_bytes() { return sizeof(float) * RING * ROWF; }
+template <bool ALPHA1, int RING>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING>);
+}
 
-FastPlan plan_fast(int nx, int rows, int batch, int device) {
+void* pick_kernel(bool alpha1, int ring) {
+  if (ring == 5) return alpha1 ? kernel_ptr<true, 5>() : kernel_ptr<false, 5>();
+  return alpha1 ? kernel_ptr<true, 4>() : kernel_ptr<false, 4>();
+}
+
+size_t fast_smem_bytes(int ring, bool general) {
+  return sizeof(float) * (ring * ROWF + (general ? 32 * 13 : 0));
+}
+
+FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general) {
   FastPlan p{};
+  p.ring = pressure ? 5 : 4;
+  p.general = general;
   p.n_strips = (nx + STRIP - 1) / STRIP;
   int sms = 148, occ = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const size_t smem = fast_smem_bytes();
-  cudaFuncSetAttribute(fast_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
-  cudaFuncSetAttribute(fast_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fast_step_kernel<true>, 32, smem);
+  const size_t smem = fast_smem_bytes(p.ring, general);
+  for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring)})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
   const int64_t slots = static_cast<int64_t>(sms) * occ;
   const int64_t columns = static_cast<int64_t>(batch) * p.n_strips;
   // choose the number of row segments maximising wave efficiency, discounting the ~0.6-row
-  // warm-up each segment pays, with segments of at least 8 rows
+  // tail each segment pays, with segments of at least 8 rows
   double best = -1.0;
   int best_segs = 1;
   const int max_segs = std::max(1, rows / 8);
@@ -609,6 +634,7 @@ FastPlan plan_fast(int nx, int rows, int batch, int device) {
   p.n_segs = (rows + p.seg_rows - 1) / p.seg_rows;
   p.units = columns * p.n_segs;
   p.smem = smem;
+  p.occupancy = occ;
   return p;
 }
 
@@ -616,13 +642,25 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
                         const FastPlan& p, cudaStream_t stream) {
   const int rows = a.u1 - a.u0;
   if (rows <= 0 || a.batch <= 0) return cudaSuccess;
-  if (f.alpha1)
-    fast_step_kernel<true><<<static_cast<unsigned>(p.units), 32, p.smem, stream>>>(
-        tmap[0], tmap[1], a, f, p.n_strips, p.seg_rows, p.n_segs);
-  else
-    fast_step_kernel<false><<<static_cast<unsigned>(p.units), 32, p.smem, stream>>>(
-        tmap[0], tmap[1], a, f, p.n_strips, p.seg_rows, p.n_segs);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.units));
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const CUtensorMap& txy = tmap[0];
+  const CUtensorMap& tz = tmap[1];
+  const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
+  if (p.ring == 5) {
+    if (f.alpha1) return cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 5>, txy, tz, a, f, ns, sr, ng);
+    return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 5>, txy, tz, a, f, ns, sr, ng);
+  }
+  if (f.alpha1) return cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 4>, txy, tz, a, f, ns, sr, ng);
+  return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4>, txy, tz, a, f, ns, sr, ng);
 }
 
 }  // namespace scb

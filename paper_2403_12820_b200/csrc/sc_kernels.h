@@ -30,11 +30,14 @@ struct FastPlan {
   int n_strips, seg_rows, n_segs;
   int64_t units;  // one single-warp CTA per (cloth, 128-column strip, row segment)
   size_t smem;
+  int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
+  bool general;   // collider / pressure / mask finish compiled in (needs per-lane scratch)
+  int occupancy;  // resident CTAs per SM
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
 bool fast_supported(const NetConst<float>& net, int nx);
-FastPlan plan_fast(int nx, int rows, int batch, int device);
+FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general);
 // tmap[0]: xy pairs of a.in as 8-byte elements, dims (pitch, rows, 2, batch), box (136,1,2,1);
 // tmap[1]: z planes, dims (pitch, rows, 2, batch) from element 4S, box (136,1,2,1).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
