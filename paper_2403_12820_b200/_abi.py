@@ -83,6 +83,7 @@ SIGNATURES = {
     "sc_ctx_advance": (C.c_int, [_P, _I, _I, C.c_int]),
     "sc_ctx_sync": (C.c_int, [_P]),
     "sc_ctx_set_health_checks": (C.c_int, [_P, _I]),
+    "sc_ctx_set_persistent": (C.c_int, [_P, _I]),
     "sc_ctx_get_health": (C.c_int, [_P, _P, _P, _P]),
     "sc_rollout": (C.c_int, [_P, _P, _P, _I, _I, C.c_int, _P, _P, _P]),
     "sc_rollout_frames": (C.c_int, [_P, _P, _P, _I, _I, C.c_int, _P, _P]),

@@ -131,6 +131,9 @@ class Context:
     def advance(self, steps: int, k0: int = 0, mode: str = "parity") -> None:
         _raise(self.lib, self.lib.sc_ctx_advance(self.h, int(steps), int(k0), MODES[mode]))
 
+    def set_persistent(self, on: bool) -> None:
+        _raise(self.lib, self.lib.sc_ctx_set_persistent(self.h, int(bool(on))))
+
     def set_health_checks(self, on: bool) -> None:
         _raise(self.lib, self.lib.sc_ctx_set_health_checks(self.h, int(bool(on))))
 

@@ -13,6 +13,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -118,6 +119,8 @@ struct sc_ctx {
   DevBuf<Health> health;
   DevBuf<uint8_t> mask;
   DevBuf<unsigned char> aos;  // staging for AoS x, v, impulse
+  DevBuf<int32_t> done;       // per-unit step counters of the persistent FAST kernel
+  bool multi_on = false;      // persistent multi-step kernel (opt-in; per-step + PDL is faster)
   // params
   NetConst<float> net32{};
   NetConst<double> net64{};
@@ -125,6 +128,7 @@ struct sc_ctx {
   bool fast_ok = false;
   FastPlan plan{};       // simple finish (no colliders / pressure / mask)
   FastPlan plan_gen{};   // general finish
+  std::map<long long, FastPlan> plan_cache;  // row-range launches of strip contexts
   bool any_pressure = false, any_general = false;
   CUtensorMap tmap[2][2];  // [buffer][xy pairs | z planes]
   bool tmap_ok = false;
@@ -149,11 +153,13 @@ void free_scene(sc_ctx* c) {
   }
   c->pin_bits.release();
   c->pin_rank.release();
+  c->done.release();
   c->health.release();
   c->mask.release();
   c->aos.release();
   c->has_scene = false;
   c->tmap_ok = false;
+  c->plan_cache.clear();
 }
 
 bool finite3(const double* v) {
@@ -427,9 +433,15 @@ void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, doubl
   if constexpr (std::is_same<T, float>::value) {
     if (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok) {
       FastPlan plan = mask ? c->plan_gen : c->plan;
-      if (u0 != c->u0 || u1 != c->u1)
-        plan = plan_fast(c->nx, u1 - u0, c->batch, c->device, c->any_pressure,
-                         c->any_general || mask != nullptr);
+      if (u0 != c->u0 || u1 != c->u1) {
+        const bool gen = c->any_general || mask != nullptr;
+        const long long key = (static_cast<long long>(u1 - u0) << 1) | (gen ? 1 : 0);
+        auto it = c->plan_cache.find(key);
+        if (it == c->plan_cache.end())
+          it = c->plan_cache.emplace(key, plan_fast(c->nx, u1 - u0, c->batch, c->device,
+                                                    c->any_pressure, gen)).first;
+        plan = it->second;
+      }
       e = launch_fast(a, c->fast, c->tmap[c->cur], plan, stream);
     } else {
       e = launch_parity<float>(a, kind, stream);
@@ -504,7 +516,26 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
   if (mode != SC_MODE_PARITY && mode != SC_MODE_FAST) throw_config("mode: unknown");
   if (mode == SC_MODE_FAST && c->prec != SC_F32)
     throw_config("mode: FAST is an f32 mode (use PARITY with an f64 context)");
-  for (int s = 0; s < steps; ++s) {
+  int s = 0;
+  // FAST: the persistent multi-step kernel for all but a mask-producing last step
+  const int multi = (mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok && c->multi_on &&
+                     c->plan.multi_ok)
+                        ? steps - (dev_mask_last ? 1 : 0)
+                        : 0;
+  if (multi >= 2) {
+    StepArgs<float> a = base_args<float>(c);
+    a.k = k0;
+    a.net = c->net32;
+    a.health = c->health_on ? c->health.p : nullptr;
+    c->done.ensure(static_cast<size_t>(c->plan.units));
+    ck(launch_fast_multi(a, c->fast, c->tmap[c->cur], c->tmap[1 - c->cur], c->plan, multi,
+                         c->done.p, c->stream),
+       "kernel launch");
+    c->launches.fetch_add(2);  // counter init + persistent kernel
+    if (multi & 1) c->cur = 1 - c->cur;
+    s = multi;
+  }
+  for (; s < steps; ++s) {
     const int k = k0 + s;
     uint8_t* m = (s == steps - 1) ? dev_mask_last : nullptr;
     if (c->prec == SC_F32)
@@ -665,6 +696,13 @@ sc_status sc_ctx_advance(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mode) {
     require_ready(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     advance_impl(c, steps, k0, mode, nullptr);
+  });
+}
+
+sc_status sc_ctx_set_persistent(sc_ctx* c, int32_t on) {
+  return guarded([&] {
+    if (!c) throw_state("null context");
+    c->multi_on = on != 0;
   });
 }
 

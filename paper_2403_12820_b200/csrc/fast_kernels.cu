@@ -308,26 +308,15 @@ __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int 
   return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * j + d] : slot[(X ? Z_X : Z_V) + j];
 }
 
+// One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
+// tensor maps and writing a.out. `phase` carries the ring barriers' parity bits across calls
+// (the persistent kernel runs many units / steps on the same ring).
 template <bool ALPHA1, int RING>
-__global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
-                                                      const __grid_constant__ CUtensorMap tmap_z,
-                                                      const StepArgs<float> a, const FastNet f,
-                                                      const int n_strips, const int seg_rows,
-                                                      const int n_segs) {
-  // dynamic smem: [RING][ROWF] ring, then (only when some cloth needs the collider / pressure /
-  // mask finish) a [32][13] per-lane impulse scratch
-  extern __shared__ __align__(128) float ring[];
-  __shared__ __align__(8) uint64_t full[RING];
-  float (*scratch)[13] = reinterpret_cast<float (*)[13]>(ring + RING * ROWF);
-
+__device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
+                                         const StepArgs<float>& a, const FastNet& f, int b,
+                                         int strip, int y0, int y1, float* ring, uint64_t* full,
+                                         float (*scratch)[13], uint32_t& phase) {
   const int lane = threadIdx.x;
-  const int unit = blockIdx.x;
-  const int seg = unit % n_segs;
-  const int strip = (unit / n_segs) % n_strips;
-  const int b = unit / (n_segs * n_strips);
-  const int y0 = a.u0 + seg * seg_rows;
-  const int y1 = min(y0 + seg_rows, a.u1);
-  if (y0 >= y1) return;
   const int x0 = strip * STRIP;
   const int ix0 = x0 + FW * lane;
   const int nx = a.nx, ny = a.ny;
@@ -337,29 +326,28 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   const int r_first = y0 - 2;
   const int r_last = y1 + 1;
 
-  if (lane == 0) {
-    for (int s = 0; s < RING; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
   auto issue = [&](int row) {  // lane 0 only
     const int t = row - r_first;
     uint64_t* bar = &full[t % RING];
     float* slot = ring + (t % RING) * ROWF;
     mbar_expect_tx(bar, ROW_BYTES);
-    tma_load_4d(slot, &tmap_xy, x0 - 4, row - a.g0, 0, b, bar);
-    tma_load_4d(slot + Z_X, &tmap_z, x0 - 4, row - a.g0, 0, b, bar);
+    tma_load_4d(slot, tmap_xy, x0 - 4, row - a.g0, 0, b, bar);
+    tma_load_4d(slot + Z_X, tmap_z, x0 - 4, row - a.g0, 0, b, bar);
   };
-  // programmatic dependent launch: everything above overlapped the previous step's tail; the
-  // state it wrote is read from here on
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  auto wait_slot = [&](int t) {
+    const int sl = t % RING;
+    mbar_wait(&full[sl], (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  __syncwarp();  // earlier generic reads of the ring are done before TMA refills it
   if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     issue(r_first);
     issue(r_first + 1);
     issue(r_first + 2);
   }
-  mbar_wait(&full[0], 0);
-  mbar_wait(&full[1], 0);
+  wait_slot(0);
+  wait_slot(1);
 
   // nx % 4 == 0 (fast_supported): only a strip's outermost lanes own edges leaving the grid
   const float mL = ix0 >= 1 ? 1.0f : 0.0f;
@@ -394,7 +382,7 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(R + 1);
     }
-    mbar_wait(&full[t % RING], (t / RING) & 1);
+    wait_slot(t);
 
     const float* rowR = ring + (t % RING) * ROWF;
     const float* row1 = ring + ((t + RING - 1) % RING) * ROWF;
@@ -549,9 +537,110 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
       Z1[k] = Z2[k];
     }
   }
+}
+
+template <bool ALPHA1, int RING>
+__global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
+                                                      const __grid_constant__ CUtensorMap tmap_z,
+                                                      const StepArgs<float> a, const FastNet f,
+                                                      const int n_strips, const int seg_rows,
+                                                      const int n_segs) {
+  // dynamic smem: [RING][ROWF] ring, then (only when some cloth needs the collider / pressure /
+  // mask finish) a [32][13] per-lane impulse scratch
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[RING];
+  float (*scratch)[13] = reinterpret_cast<float (*)[13]>(ring + RING * ROWF);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RING; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int unit = blockIdx.x;
+  const int seg = unit % n_segs;
+  const int strip = (unit / n_segs) % n_strips;
+  const int b = unit / (n_segs * n_strips);
+  const int y0 = a.u0 + seg * seg_rows;
+  const int y1 = min(y0 + seg_rows, a.u1);
+  // programmatic dependent launch: the setup above overlapped the previous step's tail; the
+  // state it wrote is read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t phase = 0;
+  if (y0 < y1)
+    run_unit<ALPHA1, RING>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch, phase);
   // let the next step's grid launch once every CTA of this one is done with its work (an early
   // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
   asm volatile("griddepcontrol.launch_dependents;");
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Persistent multi-step variant: one co-resident CTA per unit runs `steps` consecutive steps,
+// ping-ponging between the two state buffers. Instead of a grid-wide barrier per step, a unit
+// starts step k once its (up to 8) neighbour units — the only ones whose rows/columns lie within
+// the stencil's 2-node reach — published completion of step k-1 (acquire/release flags in
+// global memory). That covers both the read-after-write (halo rows of step k-1) and the
+// write-after-read (neighbours done reading the buffer this step overwrites) hazards.
+template <bool ALPHA1, int RING>
+__global__ void __launch_bounds__(32, 16) fast_multi_kernel(
+    const __grid_constant__ CUtensorMap txy0, const __grid_constant__ CUtensorMap tz0,
+    const __grid_constant__ CUtensorMap txy1, const __grid_constant__ CUtensorMap tz1,
+    const StepArgs<float> a0, const FastNet f, const int n_strips, const int seg_rows,
+    const int n_segs, const int steps, int* __restrict__ done) {
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[RING];
+  float (*scratch)[13] = reinterpret_cast<float (*)[13]>(ring + RING * ROWF);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RING; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int unit = blockIdx.x;
+  const int seg = unit % n_segs;
+  const int strip = (unit / n_segs) % n_strips;
+  const int b = unit / (n_segs * n_strips);
+  const int y0 = a0.u0 + seg * seg_rows;
+  const int y1 = min(y0 + seg_rows, a0.u1);
+  uint32_t phase = 0;
+  StepArgs<float> a = a0;
+  for (int s = 0; s < steps; ++s) {
+    const int k = a0.k + s;
+    if (s > 0 && threadIdx.x == 0) {
+      for (int dg = -1; dg <= 1; ++dg)
+        for (int ds = -1; ds <= 1; ++ds) {
+          const int g2 = seg + dg, s2 = strip + ds;
+          if ((dg == 0 && ds == 0) || g2 < 0 || g2 >= n_segs || s2 < 0 || s2 >= n_strips) continue;
+          const int* flag = done + (b * n_strips + s2) * n_segs + g2;
+          while (ld_acquire(flag) < k - 1) {
+          }
+        }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+    }
+    __syncwarp();
+    const bool even = (s & 1) == 0;
+    a.in = even ? a0.in : a0.out;
+    a.out = even ? a0.out : const_cast<float*>(a0.in);
+    a.k = k;
+    if (y0 < y1)
+      run_unit<ALPHA1, RING>(even ? &txy0 : &txy1, even ? &tz0 : &tz1, a, f, b, strip, y0, y1,
+                             ring, full, scratch, phase);
+    __syncwarp();  // orders every lane's stores before lane 0's (cumulative) release
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      st_release(done + unit, k);
+    }
+  }
+}
+
+__global__ void fill_done(int* done, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) done[i] = v;
 }
 
 }  // namespace
@@ -593,6 +682,16 @@ void* pick_kernel(bool alpha1, int ring) {
   return alpha1 ? kernel_ptr<true, 4>() : kernel_ptr<false, 4>();
 }
 
+template <bool ALPHA1, int RING>
+void* multi_ptr() {
+  return reinterpret_cast<void*>(fast_multi_kernel<ALPHA1, RING>);
+}
+
+void* pick_multi(bool alpha1, int ring) {
+  if (ring == 5) return alpha1 ? multi_ptr<true, 5>() : multi_ptr<false, 5>();
+  return alpha1 ? multi_ptr<true, 4>() : multi_ptr<false, 4>();
+}
+
 size_t fast_smem_bytes(int ring, bool general) {
   return sizeof(float) * (ring * ROWF + (general ? 32 * 13 : 0));
 }
@@ -605,7 +704,8 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   int sms = 148, occ = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = fast_smem_bytes(p.ring, general);
-  for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring)})
+  for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring), pick_multi(true, p.ring),
+                  pick_multi(false, p.ring)})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
@@ -635,6 +735,9 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   p.units = columns * p.n_segs;
   p.smem = smem;
   p.occupancy = occ;
+  int occ_multi = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_multi, pick_multi(true, p.ring), 32, smem);
+  p.multi_ok = p.units <= static_cast<int64_t>(sms) * occ_multi;  // every unit co-resident
   return p;
 }
 
@@ -661,6 +764,38 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   }
   if (f.alpha1) return cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 4>, txy, tz, a, f, ns, sr, ng);
   return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4>, txy, tz, a, f, ns, sr, ng);
+}
+
+cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tin,
+                              const CUtensorMap* tout, const FastPlan& p, int steps, int* done,
+                              cudaStream_t stream) {
+  const int rows = a.u1 - a.u0;
+  if (rows <= 0 || a.batch <= 0 || steps <= 0) return cudaSuccess;
+  const int units = static_cast<int>(p.units);
+  fill_done<<<(units + 255) / 256, 256, 0, stream>>>(done, units, a.k - 1);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(units));
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: units wait on each other
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
+  if (p.ring == 5) {
+    if (f.alpha1)
+      return cudaLaunchKernelEx(&cfg, fast_multi_kernel<true, 5>, tin[0], tin[1], tout[0],
+                                tout[1], a, f, ns, sr, ng, steps, done);
+    return cudaLaunchKernelEx(&cfg, fast_multi_kernel<false, 5>, tin[0], tin[1], tout[0], tout[1],
+                              a, f, ns, sr, ng, steps, done);
+  }
+  if (f.alpha1)
+    return cudaLaunchKernelEx(&cfg, fast_multi_kernel<true, 4>, tin[0], tin[1], tout[0], tout[1],
+                              a, f, ns, sr, ng, steps, done);
+  return cudaLaunchKernelEx(&cfg, fast_multi_kernel<false, 4>, tin[0], tin[1], tout[0], tout[1], a,
+                            f, ns, sr, ng, steps, done);
 }
 
 }  // namespace scb

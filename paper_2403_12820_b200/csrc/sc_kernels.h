@@ -33,6 +33,7 @@ struct FastPlan {
   int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
   bool general;   // collider / pressure / mask finish compiled in (needs per-lane scratch)
   int occupancy;  // resident CTAs per SM
+  bool multi_ok;  // all units fit co-resident: the persistent multi-step kernel may run
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
@@ -42,6 +43,11 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
 // tmap[1]: z planes, dims (pitch, rows, 2, batch) from element 4S, box (136,1,2,1).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
                         const FastPlan& plan, cudaStream_t stream);
+// `steps` FAST steps in one persistent launch (a.in -> a.out -> a.in ...); tin / tout: tensor
+// maps of a.in / a.out; done: per-unit step counters (plan.units ints).
+cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tin,
+                              const CUtensorMap* tout, const FastPlan& plan, int steps, int* done,
+                              cudaStream_t stream);
 
 // layout.cu: AoS [batch][node][3] <-> planar [batch][6][rows][pitch]
 // (rows = the ctx's local rows; AoS arrays hold exactly those rows.)
