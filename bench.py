@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_NODE_UPDATE = 48  # fp32 x, v: 24 B read + 24 B written per node per timestep
-CONFIG_ID = 2
+CONFIG_ID = 2  # default workload; --config 4 (row strips) / 5 (4096 cloths) also run
 
 
 def _peaks():
@@ -192,11 +192,47 @@ def run_reference(args, world, rank):
     return 0
 
 
+def _e2e_batch(cb, x, v, steps, mode, world, max_over_ranks, barrier, calls):
+    """The reference-facing C-ABI call with host buffers: sc_rollout of `steps` timesteps from
+    pinned host x0/v0 to host x/v (H2D + steps + D2H inside the timed region)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2403_12820_b200 import _abi
+
+    lib = _abi.load()
+    nbytes = x.nbytes
+    bufs = []
+    for _ in range(4):
+        ptr = C.c_void_p()
+        assert lib.sc_host_alloc(nbytes, C.byref(ptr)) == 0
+        bufs.append(ptr)
+    arrs = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), shape=x.shape) for p in bufs]
+    arrs[0][...] = x
+    arrs[1][...] = v
+    cb.rollout(arrs[0], arrs[1], 2, 0, mode)  # warm the path
+    barrier()
+    t = []
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        rc = lib.sc_rollout(cb.h, bufs[0], bufs[1], steps, 0, 1 if mode == "fast" else 0,
+                            bufs[2], bufs[3], None)
+        t.append(time.perf_counter() - t0)
+        assert rc == 0, lib.sc_last_error()
+    barrier()
+    sec = max_over_ranks(min(t))
+    finite = bool(np.isfinite(arrs[2]).all() and np.isfinite(arrs[3]).all())
+    for p in bufs:
+        lib.sc_host_free(p)
+    return sec, 2 * nbytes, 2 * nbytes, finite
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
 
-    from paper_2403_12820_b200 import ClothBatch, _abi, configs
+    from paper_2403_12820_b200 import ClothBatch, configs, strips
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -215,78 +251,109 @@ def run_ours(args, world, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    cfg = configs.CONFIGS[CONFIG_ID]
-    B = cfg.batch
-    _, scenes, params, x, v = configs.build(CONFIG_ID, batch=B, cloth0=rank * B)
-    nodes_rank = B * cfg.n * cfg.n
+    cid = args.config
+    cfg = configs.CONFIGS[cid]
     mode = args.mode
-    cb = ClothBatch(scenes, params, device=local)
-    cb.set_state(x, v)
-    cb.advance(args.warmup, 0, mode)
-    cb.sync()
-
-    # ---- timed region: K fused steps, device-timed with CUDA events on the ctx stream ----
-    barrier()
-    launches0 = cb.launch_count()
-    with ClockSampler(local) as clocks:
-        sec = cb.benchmark(args.steps, 0, mode)  # events around exactly K launches
-        cb.sync()
-    launches = cb.launch_count() - launches0
-    barrier()
-    sec_max = max_over_ranks(sec)
-    value = world * nodes_rank * args.steps / sec_max
-
-    # ---- roofline of the dominant (only) kernel: per-launch events over the same work ----
-    launch_ms = cb.benchmark_launches(min(args.steps, 20), args.warmup + args.steps, mode)
-    avg_launch_s = float(np.mean(launch_ms)) * 1e-3
-    achieved = BYTES_PER_NODE_UPDATE * nodes_rank / avg_launch_s / 1e9
     peak, peak_src = _peaks()
     kernel = "fast_step_kernel" if mode == "fast" else "parity_kernel"
-    workload = "cfg2_64x256x256"
+    extra = {}
+    if cid in (2, 5):
+        # ---- batch sharding: every rank owns the config's batch (cloth ids B*rank ..) ----
+        B = cfg.batch
+        _, scenes, params, x, v = configs.build(cid, batch=B, cloth0=rank * B)
+        nodes_rank = B * cfg.n * cfg.n
+        cb = ClothBatch(scenes, params, device=local)
+        cb.set_state(x, v)
+        cb.advance(args.warmup, 0, mode)
+        cb.sync()
+        barrier()
+        launches0 = cb.launch_count()
+        with ClockSampler(local) as clocks:
+            sec = cb.benchmark(args.steps, 0, mode)  # CUDA events around exactly K launches
+            cb.sync()
+        launches = cb.launch_count() - launches0
+        barrier()
+        sec_max = max_over_ranks(sec)
+        # the fused kernel is the only launch per step: its average duration over the timed
+        # region is region / launches (inter-launch gaps included, i.e. conservative)
+        avg_launch_s = sec / max(launches, 1)
+        cb.set_state(x, v)
+        ps = max(5, min(args.steps, 20))
+        parity_value = world * nodes_rank * ps / cb.benchmark(ps, 2, "parity")
+        extra["parity_mode"] = {"value": parity_value, "unit": "node-updates/s",
+                                "note": "bit-exact with the reference f32 templates"}
+        e2e_steps = cfg.steps
+        e2e_sec, hb, db, finite = _e2e_batch(cb, x, v, e2e_steps, mode, world, max_over_ranks,
+                                             barrier, args.e2e_calls)
+        e2e = {"value": world * nodes_rank * e2e_steps / e2e_sec, "unit": "node-updates/s",
+               "h2d_bytes_per_step": hb / e2e_steps, "d2h_bytes_per_step": db / e2e_steps,
+               "call": "sc_rollout host->host, %d timesteps per call (pinned buffers)"
+                       % e2e_steps, "finite": finite}
+        cb.close()
+        conf = {"workload": "cfg%d: %s" % (cid, cfg.description), "cloths_per_gpu": B,
+                "grid": "%dx%d" % (cfg.n, cfg.n), "nodes_per_gpu": nodes_rank,
+                "timesteps_per_step": 1, "mode": mode,
+                "l2": "no flush: ping-pong state 2 x %.1f MB > 126 MB L2" % (24e-6 * nodes_rank),
+                "parallelism": "dp%d batch-sharded, no collective" % world}
+        scaling = "weak"
+    elif cid == 4:
+        # ---- one 8192^2 cloth in row strips, halo rows over NCCL each step ----
+        row0, rows = strips.strip_bounds(cfg.n, world, rank)
+        g0, g1 = strips.local_window(cfg.n, row0, rows)
+        xl, _ = configs.sheet(cfg.seed, 0, cfg.n, g0, g1 - g0)
+        scene = configs.make_scene(cfg, 0, xl.astype(np.float64), row0=g0)
+        params = configs.make_params(cfg.seed, cfg.hidden8)
+        sr = strips.StripRollout(scene, params, xl, np.zeros_like(xl), rank, world, local,
+                                 mode=mode)
+        nodes_rank = rows * cfg.n
+        for k in range(args.warmup):
+            sr.step(k)
+        barrier()
+        l0 = sr.ctx.launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clocks:
+            ev0.record(sr.stream)
+            for k in range(args.warmup, args.warmup + args.steps):
+                sr.step(k)
+            ev1.record(sr.stream)
+            ev1.synchronize()
+        launches = sr.ctx.launch_count() - l0
+        barrier()
+        sec = ev0.elapsed_time(ev1) * 1e-3
+        sec_max = max_over_ranks(sec)
+        avg_launch_s = sec / args.steps  # one interior launch dominates each step
+        t0 = time.perf_counter()
+        sr.ctx.set_state(xl, np.zeros_like(xl))
+        for k in range(args.steps):
+            sr.step(k)
+        sr.state()
+        e2e_sec = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * nodes_rank * args.steps / e2e_sec, "unit": "node-updates/s",
+               "h2d_bytes_per_step": 2 * xl.nbytes / args.steps,
+               "d2h_bytes_per_step": 2 * xl.nbytes / args.steps,
+               "call": "set_state (host) + %d strip steps + get_state (host)" % args.steps}
+        sr.close()
+        conf = {"workload": "cfg4: " + cfg.description, "grid": "8192x8192",
+                "nodes_per_gpu": nodes_rank, "timesteps_per_step": 1, "mode": mode,
+                "l2": "no flush: state 2 x %.0f MB >> 126 MB L2" % (24e-6 * nodes_rank),
+                "parallelism": "%d row strips, 2-row halo per step over NCCL" % world}
+        scaling = "strong"
+    else:
+        raise SystemExit("--config must be 2, 4 or 5")
+
+    value = world * nodes_rank * args.steps / sec_max if cid != 4 else \
+        cfg.n * cfg.n * args.steps / sec_max
+    achieved = BYTES_PER_NODE_UPDATE * nodes_rank / avg_launch_s / 1e9
+    workload = {2: "cfg2_64x256x256", 4: "cfg4_8192x8192", 5: "cfg5_4096x128x128"}[cid]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": _traffic(kernel, workload),
                 "kernel": kernel, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": BYTES_PER_NODE_UPDATE * nodes_rank,
                 "avg_launch_ms": avg_launch_s * 1e3}
 
-    # ---- PARITY (bit-exact) mode throughput, short, for reference ----
-    parity_sec = cb.benchmark(max(5, min(args.steps, 20)), 2, "parity")
-    parity_value = nodes_rank * max(5, min(args.steps, 20)) / parity_sec * world
-
-    # ---- e2e: the reference-facing C-ABI call with HOST buffers: sc_rollout of the config's
-    #      full length (cfg.steps timesteps) from pinned host x0/v0 to host x/v ----
-    lib = _abi.load()
-    nbytes = x.nbytes
-    bufs = []
-    for _ in range(4):
-        import ctypes as C
-        ptr = C.c_void_p()
-        assert lib.sc_host_alloc(nbytes, C.byref(ptr)) == 0
-        bufs.append(ptr)
-    import ctypes as C
-    arrs = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), shape=x.shape) for p in bufs]
-    arrs[0][...] = x
-    arrs[1][...] = v
-    e2e_steps = cfg.steps
-    cb.rollout(arrs[0], arrs[1], 2, 0, mode)  # warm the path
-    barrier()
-    t_e2e = []
-    for _ in range(args.e2e_calls):
-        t0 = time.perf_counter()
-        rc = lib.sc_rollout(cb.h, bufs[0], bufs[1], e2e_steps, 0, 1 if mode == "fast" else 0,
-                            bufs[2], bufs[3], None)
-        t_e2e.append(time.perf_counter() - t0)
-        assert rc == 0, lib.sc_last_error()
-    barrier()
-    e2e_sec = max_over_ranks(min(t_e2e))
-    e2e_value = world * nodes_rank * e2e_steps / e2e_sec
-    finite = bool(np.isfinite(arrs[2]).all() and np.isfinite(arrs[3]).all())
-    for p in bufs:
-        lib.sc_host_free(p)
-
     # ---- CPU baseline: reference CPU path on this host, bounded sample (rank 0, N=1) ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cid == 2:
         try:
             from oracle.pyoracle import Reference
             ref = Reference()
@@ -307,26 +374,13 @@ def run_ours(args, world, rank, local):
             "metric": "cloth node-updates/s", "value": value, "unit": "node-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sec_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg2: " + cfg.description, "cloths_per_gpu": B,
-                       "grid": "256x256", "nodes_per_gpu": nodes_rank, "timesteps_per_step": 1,
-                       "mode": mode, "l2": "no flush: ping-pong state 2 x 100.7 MB > 126 MB L2",
-                       "parallelism": "dp%d batch-sharded, no collective" % world},
-            "roofline": roofline,
-            "hbm_fraction": achieved / peak,
-            "parity_mode": {"value": parity_value, "unit": "node-updates/s",
-                            "note": "bit-exact with the reference f32 templates"},
-            "e2e": {"value": e2e_value, "unit": "node-updates/s",
-                    "h2d_bytes_per_step": 2 * nbytes / e2e_steps,
-                    "d2h_bytes_per_step": 2 * nbytes / e2e_steps,
-                    "call": "sc_rollout host->host, %d timesteps per call (pinned buffers)"
-                            % e2e_steps, "finite": finite},
-            "gpu_launches": int(launches),
-            "clocks": clocks.summary(),
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": conf, "roofline": roofline, "hbm_fraction": achieved / peak,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
-    cb.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
@@ -339,6 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
+    ap.add_argument("--config", type=int, choices=[2, 4, 5], default=CONFIG_ID)
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -22,6 +22,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sc_device.cuh"
 #include "sc_kernels.h"
@@ -731,6 +732,10 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
     }
   }
   p.seg_rows = (rows + best_segs - 1) / best_segs;
+  if (const char* env = std::getenv("SC_FAST_SEG_ROWS")) {  // tuning knob for experiments
+    const int v = std::atoi(env);
+    if (v >= 2) p.seg_rows = std::min(v, rows);
+  }
   p.n_segs = (rows + p.seg_rows - 1) / p.seg_rows;
   p.units = columns * p.n_segs;
   p.smem = smem;

@@ -82,11 +82,16 @@ class StripRollout:
         dev = torch.device("cuda", device)
         self.send_lo, self.send_hi, self.recv_lo, self.recv_hi = (
             torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(4))
+        # a real (non-legacy) stream: kernels, packs and NCCL all order on it
+        self.stream = torch.cuda.Stream(device=dev)
 
     def step(self, k: int) -> None:
         import torch
 
-        stream = torch.cuda.current_stream().cuda_stream
+        with torch.cuda.stream(self.stream):
+            self._step(k, self.stream.cuda_stream)
+
+    def _step(self, k: int, stream: int) -> None:
         r0, r1 = self.row0, self.row0 + self.rows
         lo_end = min(r1, r0 + HALO) if self.rank > 0 else r0
         hi_beg = max(lo_end, r1 - HALO) if self.rank < self.world - 1 else r1
@@ -115,9 +120,7 @@ class StripRollout:
         self.ctx.strip_commit()
 
     def state(self):
-        import torch
-
-        torch.cuda.current_stream().synchronize()
+        self.stream.synchronize()
         return self.ctx.get_state()
 
     def close(self) -> None:
