@@ -120,8 +120,8 @@ def _traffic(kernel: str, workload: str):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(kernel, {})
-        if e.get("workload") == workload:
+        e = t.get(workload) if kernel == "fast_step_kernel" else t.get(kernel + ":" + workload)
+        if e and e.get("workload") == workload:
             return e.get("dram_bytes_per_launch")
     except Exception:
         pass

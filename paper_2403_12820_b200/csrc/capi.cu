@@ -983,12 +983,12 @@ sc_status sc_ctx_strip_step(sc_ctx* c, int32_t k, int32_t r_begin, int32_t r_end
       throw_config("strip_step: rows outside the owned strip");
     if (mode == SC_MODE_FAST && c->prec != SC_F32) throw_config("mode: FAST is an f32 mode");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    Health* h = c->health_on ? c->health.p : nullptr;
     if (c->prec == SC_F32)
-      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, c->health.p, r_begin,
-                        r_end, st);
+      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, h, r_begin, r_end, st);
     else
-      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, c->health.p,
-                         r_begin, r_end, st);
+      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, h, r_begin, r_end,
+                         st);
   });
 }
 
