@@ -135,19 +135,25 @@ def _cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+_REF_INPUTS = {}
+
+
 def reference_sample(ref, cores: int, steps: int, warmup: int = 1, cloth0: int = 0):
     """benchmark_net (eval.cpp:155-158) on `cores` config-2 cloths, one thread each (the
-    cloth-parallel variant: reference code unchanged, global thread count 1)."""
+    cloth-parallel variant: reference code unchanged, global thread count 1). Inputs are
+    generated once per (cores, cloth0) and reused across samples."""
     from paper_2403_12820_b200 import configs
     import numpy as np
 
-    cfg, scenes, p, x, v = configs.build(CONFIG_ID, batch=cores, cloth0=cloth0)
-    keep: list = []
-    cds = [s.cloth_desc(keep) for s in scenes]
-    x64 = np.ascontiguousarray(x, np.float64)
-    v64 = np.ascontiguousarray(v, np.float64)
-    mx, wall = ref.benchmark_net_cloth_parallel(cfg.n, cfg.n, cds, p.to_c(), x64, v64, steps,
-                                                warmup)
+    key = (cores, cloth0)
+    if key not in _REF_INPUTS:
+        cfg, scenes, p, x, v = configs.build(CONFIG_ID, batch=cores, cloth0=cloth0)
+        keep: list = []
+        cds = [s.cloth_desc(keep) for s in scenes]
+        _REF_INPUTS[key] = (cfg, cds, keep, p.to_c(), np.ascontiguousarray(x, np.float64),
+                            np.ascontiguousarray(v, np.float64))
+    cfg, cds, _, pc, x64, v64 = _REF_INPUTS[key]
+    mx, wall = ref.benchmark_net_cloth_parallel(cfg.n, cfg.n, cds, pc, x64, v64, steps, warmup)
     nodes = cores * cfg.n * cfg.n * steps
     return nodes, mx, wall
 
@@ -161,10 +167,12 @@ def run_reference(args, world, rank):
     cfg = configs.CONFIGS[CONFIG_ID]
     ref = Reference()
     cores = _cpu_cores()
-    # calibrate the per-sample timestep count to ~1 s of CPU time per bench step
+    # size every step's sample so the whole --steps K --warmup W run takes ~args.ref_budget
+    # seconds of CPU time (each step: `cores` cloths x ts timesteps, ts >= 1)
     n0, s0, _ = reference_sample(ref, cores, 2, 1)
     per_ts = s0 / 2
-    ts = max(1, min(200, int(round(1.0 / max(per_ts, 1e-6)))))
+    per_step = args.ref_budget / max(1, args.steps + args.warmup)
+    ts = max(1, min(200, int(per_step / max(per_ts, 1e-6))))
     for _ in range(args.warmup):
         reference_sample(ref, cores, ts, 0)
     total_nodes, total_sec, times = 0, 0.0, []
@@ -397,6 +405,8 @@ def main():
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="CPU seconds for the whole --impl reference run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

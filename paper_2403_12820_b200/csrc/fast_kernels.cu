@@ -612,16 +612,19 @@ __global__ void __launch_bounds__(32, 16) fast_multi_kernel(
   StepArgs<float> a = a0;
   for (int s = 0; s < steps; ++s) {
     const int k = a0.k + s;
-    if (s > 0 && threadIdx.x == 0) {
-      for (int dg = -1; dg <= 1; ++dg)
-        for (int ds = -1; ds <= 1; ++ds) {
-          const int g2 = seg + dg, s2 = strip + ds;
-          if ((dg == 0 && ds == 0) || g2 < 0 || g2 >= n_segs || s2 < 0 || s2 >= n_strips) continue;
+    if (s > 0) {
+      // lanes 0..8 each watch one neighbour (all polled concurrently: one L2 round trip)
+      if (threadIdx.x < 9 && threadIdx.x != 4) {
+        const int dg = static_cast<int>(threadIdx.x) / 3 - 1, ds = static_cast<int>(threadIdx.x) % 3 - 1;
+        const int g2 = seg + dg, s2 = strip + ds;
+        if (g2 >= 0 && g2 < n_segs && s2 >= 0 && s2 < n_strips) {
           const int* flag = done + (b * n_strips + s2) * n_segs + g2;
           while (ld_acquire(flag) < k - 1) {
           }
         }
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+      }
+      __syncwarp();
+      if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncwarp();
     const bool even = (s & 1) == 0;
@@ -694,7 +697,9 @@ void* pick_multi(bool alpha1, int ring) {
 }
 
 size_t fast_smem_bytes(int ring, bool general) {
-  return sizeof(float) * (ring * ROWF + (general ? 32 * 13 : 0));
+  size_t pad = 0;
+  if (const char* env = std::getenv("SC_FAST_SMEM_PAD")) pad = std::strtoul(env, nullptr, 10);
+  return sizeof(float) * (ring * ROWF + (general ? 32 * 13 : 0)) + pad;  // pad: tuning knob
 }
 
 FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general) {
