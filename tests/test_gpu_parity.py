@@ -273,3 +273,39 @@ def test_fast_persistent_kernel_matches_per_step_launches(cfg_id, n, batch, step
         lb = cb.launch_count() - la
     assert bits_equal(xa, xb) and bits_equal(va, vb)
     assert lb >= steps  # the per-step path really launched per step
+
+
+def test_fast_general_alpha_and_pair_gains(oracle):
+    """FAST mode with alpha != 1 and non-unit gains that are equal within each channel pair
+    (the channel-pair sharing precondition): the ALPHA1 = false kernel variant, per step within
+    tolerance, masks identical. Unequal pair gains fall back to the (bit-exact) PARITY kernel."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    from paper_2403_12820_b200.scene import NEGATED_CHANNEL
+    cfg, scenes, p, x, v = configs.build(3, batch=1, n=96)
+    rng = np.random.default_rng(3)
+    gains = rng.uniform(0.6, 1.4, 12)
+    for c in range(12):
+        gains[NEGATED_CHANNEL[c]] = gains[min(c, NEGATED_CHANNEL[c])]
+    p.kernel_gain = gains
+    p.isru_alpha = 1.7
+    keep = []
+    cds = [s.cloth_desc(keep) for s in scenes]
+    xs, vs, _ = oracle.rollout(96, 96, cds, p.to_c(), x, v, 4)
+    xo, vo, mo = oracle.rollout(96, 96, cds, p.to_c(), xs, vs, 1, 4)
+    with ClothBatch(scenes, p) as cb:
+        l0 = cb.launch_count()
+        xf, vf, mf = cb.rollout(xs, vs, 1, 4, "fast", constrained=True)
+    okx, ex = fast_close(xf, xo)
+    okv, ev = fast_close(vf, vo)
+    assert okx and okv, "rel err x %.3g v %.3g" % (ex, ev)
+    assert np.array_equal(mf, mo)
+    # the FAST result is not bit-identical to PARITY here (it really ran the FAST kernel)
+    assert not (bits_equal(xf, xo) and bits_equal(vf, vo))
+    # unequal pair gains: FAST requests run the bit-exact PARITY kernel instead
+    p.kernel_gain = rng.uniform(0.6, 1.4, 12)
+    keep = []
+    cds = [s.cloth_desc(keep) for s in scenes]
+    xo2, vo2, _ = oracle.rollout(96, 96, cds, p.to_c(), xs, vs, 1, 4)
+    with ClothBatch(scenes, p) as cb:
+        xf2, vf2 = cb.rollout(xs, vs, 1, 4, "fast")
+    assert bits_equal(xf2, xo2) and bits_equal(vf2, vo2)
