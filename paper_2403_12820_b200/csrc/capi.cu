@@ -527,7 +527,7 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
     a.k = k0;
     a.net = c->net32;
     a.health = c->health_on ? c->health.p : nullptr;
-    c->done.ensure(static_cast<size_t>(c->plan.units));
+    c->done.ensure(static_cast<size_t>(c->plan.n_strips) * c->batch * c->plan.multi_segs);
     ck(launch_fast_multi(a, c->fast, c->tmap[c->cur], c->tmap[1 - c->cur], c->plan, multi,
                          c->done.p, c->stream),
        "kernel launch");
@@ -1026,5 +1026,12 @@ void sc_host_free(void* p) {
 }
 
 int64_t sc_ctx_launch_count(sc_ctx* c) { return c ? c->launches.load() : 0; }
+
+// Debug instrumentation (not part of the public header): per-unit globaltimer stamps of the
+// FAST kernel into a device buffer of 2 * units uint64 (nullptr switches it off).
+sc_status sc_debug_unit_timing(void* dev_buf) {
+  return guarded([&] { ck(set_unit_timing(static_cast<unsigned long long*>(dev_buf)), "timing"); });
+}
+int64_t sc_debug_units(sc_ctx* c) { return c ? c->plan.units : 0; }
 
 }  // extern "C"

@@ -540,8 +540,27 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   }
 }
 
+__device__ unsigned long long* g_unit_times = nullptr;  // debug: [units][2] globaltimer
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Unit u -> (cloth b, strip, rows [y0, y1)); segment boundaries are spread evenly so no unit
+// gets a runt remainder.
+__device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, int u0, int rows,
+                                            int& b, int& strip, int& y0, int& y1) {
+  const int seg = unit % n_segs;
+  strip = (unit / n_segs) % n_strips;
+  b = unit / (n_segs * n_strips);
+  y0 = u0 + static_cast<int>((static_cast<int64_t>(seg) * rows) / n_segs);
+  y1 = u0 + static_cast<int>((static_cast<int64_t>(seg + 1) * rows) / n_segs);
+}
+
 template <bool ALPHA1, int RING>
-__global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
+__global__ void __launch_bounds__(32, 16) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
@@ -557,17 +576,18 @@ __global__ void __launch_bounds__(32) fast_step_kernel(const __grid_constant__ C
   }
   __syncwarp();
   const int unit = blockIdx.x;
-  const int seg = unit % n_segs;
-  const int strip = (unit / n_segs) % n_strips;
-  const int b = unit / (n_segs * n_strips);
-  const int y0 = a.u0 + seg * seg_rows;
-  const int y1 = min(y0 + seg_rows, a.u1);
+  int b, strip, y0, y1;
+  decode_unit(unit, n_strips, n_segs, a.u0, a.u1 - a.u0, b, strip, y0, y1);
+  (void)seg_rows;
   // programmatic dependent launch: the setup above overlapped the previous step's tail; the
   // state it wrote is read from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t phase = 0;
+  unsigned long long* times = g_unit_times;
+  if (times && threadIdx.x == 0) times[2 * unit] = gtimer();
   if (y0 < y1)
     run_unit<ALPHA1, RING>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch, phase);
+  if (times && threadIdx.x == 0) times[2 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
   // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -589,7 +609,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // global memory). That covers both the read-after-write (halo rows of step k-1) and the
 // write-after-read (neighbours done reading the buffer this step overwrites) hazards.
 template <bool ALPHA1, int RING>
-__global__ void __launch_bounds__(32, 16) fast_multi_kernel(
+__global__ void __launch_bounds__(32, 12) fast_multi_kernel(
     const __grid_constant__ CUtensorMap txy0, const __grid_constant__ CUtensorMap tz0,
     const __grid_constant__ CUtensorMap txy1, const __grid_constant__ CUtensorMap tz1,
     const StepArgs<float> a0, const FastNet f, const int n_strips, const int seg_rows,
@@ -604,10 +624,8 @@ __global__ void __launch_bounds__(32, 16) fast_multi_kernel(
   __syncwarp();
   const int unit = blockIdx.x;
   const int seg = unit % n_segs;
-  const int strip = (unit / n_segs) % n_strips;
-  const int b = unit / (n_segs * n_strips);
-  const int y0 = a0.u0 + seg * seg_rows;
-  const int y1 = min(y0 + seg_rows, a0.u1);
+  int b, strip, y0, y1;
+  decode_unit(unit, n_strips, n_segs, a0.u0, a0.u1 - a0.u0, b, strip, y0, y1);
   uint32_t phase = 0;
   StepArgs<float> a = a0;
   for (int s = 0; s < steps; ++s) {
@@ -723,31 +741,42 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   int best_segs = 1;
   const int max_segs = std::max(1, rows / 8);
   for (int segs = 1; segs <= max_segs && segs <= 4096; ++segs) {
-    const int seg_rows = (rows + segs - 1) / segs;
-    const int real_segs = (rows + seg_rows - 1) / seg_rows;
-    const int64_t units = columns * real_segs;
+    // segments of floor/ceil(rows / segs) rows (decode_unit spreads the boundaries evenly)
+    const double seg_rows = static_cast<double>(rows) / segs;
+    const int64_t units = columns * segs;
     const int64_t waves = (units + slots - 1) / slots;
     const double fill = static_cast<double>(units) / static_cast<double>(waves * slots);
-    const double work = static_cast<double>(rows) / (static_cast<double>(real_segs) * seg_rows);
-    const double warm = static_cast<double>(seg_rows) / (seg_rows + 0.6);
-    const double eff = fill * work * warm;
+    const double warm = seg_rows / (seg_rows + 0.6);
+    const double eff = fill * warm;
     if (eff > best + 1e-9) {
       best = eff;
-      best_segs = real_segs;
+      best_segs = segs;
     }
   }
   p.seg_rows = (rows + best_segs - 1) / best_segs;
   if (const char* env = std::getenv("SC_FAST_SEG_ROWS")) {  // tuning knob for experiments
     const int v = std::atoi(env);
-    if (v >= 2) p.seg_rows = std::min(v, rows);
+    if (v >= 2) best_segs = std::max(1, (rows + v - 1) / v);
+    p.seg_rows = (rows + best_segs - 1) / best_segs;
   }
-  p.n_segs = (rows + p.seg_rows - 1) / p.seg_rows;
+  p.n_segs = best_segs;
   p.units = columns * p.n_segs;
   p.smem = smem;
   p.occupancy = occ;
   int occ_multi = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_multi, pick_multi(true, p.ring), 32, smem);
   p.multi_ok = p.units <= static_cast<int64_t>(sms) * occ_multi;  // every unit co-resident
+  if (!p.multi_ok && occ_multi > 0) {
+    // the persistent kernel's own segmentation: one co-resident unit per slot
+    const int64_t mslots = static_cast<int64_t>(sms) * occ_multi;
+    const int msegs = static_cast<int>(std::max<int64_t>(1, mslots / columns));
+    if (columns * std::min(msegs, max_segs) <= mslots) {
+      p.multi_segs = std::min(msegs, max_segs);
+      p.multi_ok = true;
+    }
+  } else {
+    p.multi_segs = p.n_segs;
+  }
   return p;
 }
 
@@ -776,12 +805,16 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4>, txy, tz, a, f, ns, sr, ng);
 }
 
+cudaError_t set_unit_timing(unsigned long long* dev_buf) {
+  return cudaMemcpyToSymbol(g_unit_times, &dev_buf, sizeof(dev_buf));
+}
+
 cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tin,
                               const CUtensorMap* tout, const FastPlan& p, int steps, int* done,
                               cudaStream_t stream) {
   const int rows = a.u1 - a.u0;
   if (rows <= 0 || a.batch <= 0 || steps <= 0) return cudaSuccess;
-  const int units = static_cast<int>(p.units);
+  const int units = static_cast<int>(p.n_strips * static_cast<int64_t>(a.batch) * p.multi_segs);
   fill_done<<<(units + 255) / 256, 256, 0, stream>>>(done, units, a.k - 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(units));
@@ -793,7 +826,7 @@ cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
+  const int ns = p.n_strips, sr = p.seg_rows, ng = p.multi_segs;
   if (p.ring == 5) {
     if (f.alpha1)
       return cudaLaunchKernelEx(&cfg, fast_multi_kernel<true, 5>, tin[0], tin[1], tout[0],

@@ -34,6 +34,7 @@ struct FastPlan {
   bool general;   // collider / pressure / mask finish compiled in (needs per-lane scratch)
   int occupancy;  // resident CTAs per SM
   bool multi_ok;  // all units fit co-resident: the persistent multi-step kernel may run
+  int multi_segs; // segments per strip column of the persistent kernel (co-resident units)
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
@@ -45,6 +46,8 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
                         const FastPlan& plan, cudaStream_t stream);
 // `steps` FAST steps in one persistent launch (a.in -> a.out -> a.in ...); tin / tout: tensor
 // maps of a.in / a.out; done: per-unit step counters (plan.units ints).
+// debug: record [unit][start, end] globaltimer ns of every fast_step_kernel unit (nullptr: off)
+cudaError_t set_unit_timing(unsigned long long* dev_buf);
 cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tin,
                               const CUtensorMap* tout, const FastPlan& plan, int steps, int* done,
                               cudaStream_t stream);
