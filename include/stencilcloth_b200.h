@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 1
+#define SC_ABI_VERSION 2
 #define SC_CHANNELS 12 /* kChannels, include/cloth/grid.hpp:13 */
 
 typedef enum {
@@ -101,6 +101,12 @@ typedef struct {
   const sc_sphere* spheres;
   int32_t n_planes;
   const sc_plane* planes;
+  /* Material of the ground-truth mass-spring step (PBS); unused by the
+   * network step: spring stiffness and damping (MaterialParams, grid.hpp:65-76) and the grid
+   * spacing that sets the rest lengths (spacing * {1, sqrt2, 2}, grid.cpp:14-30,93-95). */
+  double stiffness; /* >= 0 */
+  double damping;   /* >= 0 */
+  double spacing;   /* > 0 when stepping PBS */
 } sc_cloth_desc;
 
 /* A batch of cloths sharing one nx-by-ny grid topology (build_grid, src/grid.cpp:83-138). */
@@ -174,6 +180,22 @@ sc_status sc_advance_with_impulse(sc_ctx* ctx, const void* x, const void* v, con
 /* nn_step (net.hpp:129-130 / net.cpp:242-248) fused, with the optional constrained mask. */
 sc_status sc_nn_step(sc_ctx* ctx, const void* x, const void* v, double t_next, sc_mode mode,
                      void* x_out, void* v_out, uint8_t* constrained);
+
+/* ---- ground-truth mass-spring step (PBS; §8(f2)), PARITY only ---------------------------- */
+/* total_impulse (sim.hpp:32 / kernels.hpp:165-175): elastic + damping + pressure + external
+ * forces scaled by dt/m, [batch][node][3]. A coincident connected pair is SC_ERR_NUMERICS
+ * naming the first node ("elastic force: singular spring ...", kernels.hpp:105-107). */
+sc_status sc_total_impulse(sc_ctx* ctx, const void* x, const void* v, void* impulse);
+/* step_semi_implicit (sim.hpp:58 / sim.cpp:150-155) from host state to host state. */
+sc_status sc_pbs_step(sc_ctx* ctx, const void* x, const void* v, double t_next, void* x_out,
+                      void* v_out, uint8_t* constrained);
+/* simulate_scene's stepping (sim.cpp:157-175) with frame storage like sc_rollout_frames; after
+ * it, sc_ctx_get_health reports the first frame whose state went non-finite (state frame) and
+ * the first singular spring (impulse frame / node). */
+sc_status sc_simulate_frames(sc_ctx* ctx, const void* x0, const void* v0, int32_t steps,
+                             int32_t stride, void* frames_x, void* frames_v);
+/* benchmark_sim (eval.hpp:46 / eval.cpp:151-153): device-timed PBS steps from the ctx state. */
+sc_status sc_benchmark_sim(sc_ctx* ctx, int32_t steps, int32_t warmup, double* seconds);
 
 /* benchmark_net (eval.hpp:47-48 / eval.cpp:69-82,155-158): warmup untimed steps then `steps`
  * timed steps from the ctx state, timed with CUDA events on the ctx stream. */

@@ -57,6 +57,10 @@ class Oracle:
             for fn in ("orc_forward_impulse_", "orc_plug_impulse_", "orc_advance_with_impulse_",
                        "orc_nn_step_", "orc_rollout_"):
                 getattr(self.lib, fn + sfx).restype = None
+            getattr(self.lib, "orc_total_impulse_" + sfx).argtypes = [_I, _I, _CD, _P, _P, _P]
+            getattr(self.lib, "orc_total_impulse_" + sfx).restype = C.c_long
+            getattr(self.lib, "orc_pbs_step_" + sfx).argtypes = [_I, _I, _CD, _P, _P, T, _P, _P, _P]
+            getattr(self.lib, "orc_pbs_step_" + sfx).restype = C.c_long
 
     @staticmethod
     def _dt(a):
@@ -88,6 +92,22 @@ class Oracle:
             nx, ny, C.byref(cloth), C.byref(params), _p(x), _p(v), t_next, _p(xo), _p(vo), _p(m),
             _p(imp))
         return xo, vo, m, imp
+
+    def total_impulse(self, nx, ny, cloth, x, v):
+        """(impulse, first singular node or -1)."""
+        out = np.empty_like(x)
+        sing = getattr(self.lib, "orc_total_impulse_" + self._dt(x))(nx, ny, C.byref(cloth), _p(x),
+                                                                     _p(v), _p(out))
+        return out, int(sing)
+
+    def pbs_step(self, nx, ny, cloth, x, v, t_next):
+        """step_semi_implicit: (x', v', mask, first singular node or -1)."""
+        xo, vo = np.empty_like(x), np.empty_like(v)
+        m = np.zeros(nx * ny, np.uint8)
+        sing = getattr(self.lib, "orc_pbs_step_" + self._dt(x))(nx, ny, C.byref(cloth), _p(x),
+                                                                _p(v), t_next, _p(xo), _p(vo),
+                                                                _p(m))
+        return xo, vo, m, int(sing)
 
     def rollout(self, nx, ny, cloths, params, x, v, steps, k0=0):
         """run_steps<T> sequence over a batch; returns (x, v, last-step mask)."""
@@ -121,6 +141,11 @@ class Reference:
         L.ref_rollout_f64.argtypes = [_I, _I, _CD, _PR, _P, _P, _I, _P, _P]
         L.ref_benchmark_net.argtypes = [_I, _I, _CD, _PR, _P, _P, _I, _I, _I, _I,
                                         C.POINTER(C.c_double)]
+        L.ref_total_impulse_f64.argtypes = [_I, _I, _CD, _P, _P, _P]
+        L.ref_pbs_step_f64.argtypes = [_I, _I, _CD, _P, _P, C.c_double, _P, _P]
+        L.ref_simulate_f64.argtypes = [_I, _I, _CD, _P, _P, _I, _P, _P]
+        L.ref_pbs_rollout_f32.argtypes = [_I, _I, _CD, _P, _P, _I, _I]
+        L.ref_benchmark_sim.argtypes = [_I, _I, _CD, _P, _P, _I, _I, _I, _I, C.POINTER(C.c_double)]
         L.ref_benchmark_net_cloth_parallel.argtypes = [_I, _I, _I, _CD, _PR, _P, _P, _I, _I,
                                                        C.POINTER(C.c_double),
                                                        C.POINTER(C.c_double)]
@@ -191,6 +216,37 @@ class Reference:
         self._ck(self.lib.ref_rollout_f64(nx, ny, C.byref(cloth), C.byref(params), _p(x0), _p(v0),
                                           steps, _p(fx), _p(fv)))
         return fx, fv
+
+    def total_impulse_f64(self, nx, ny, cloth, x, v):
+        out = np.empty_like(x)
+        self._ck(self.lib.ref_total_impulse_f64(nx, ny, C.byref(cloth), _p(x), _p(v), _p(out)))
+        return out
+
+    def pbs_step_f64(self, nx, ny, cloth, x, v, t_next):
+        xo, vo = np.empty_like(x), np.empty_like(v)
+        self._ck(self.lib.ref_pbs_step_f64(nx, ny, C.byref(cloth), _p(x), _p(v), t_next, _p(xo),
+                                           _p(vo)))
+        return xo, vo
+
+    def simulate_f64(self, nx, ny, cloth, x0, v0, steps):
+        n = nx * ny
+        fx = np.empty((steps + 1, n, 3))
+        fv = np.empty_like(fx)
+        self._ck(self.lib.ref_simulate_f64(nx, ny, C.byref(cloth), _p(x0), _p(v0), steps, _p(fx),
+                                           _p(fv)))
+        return fx, fv
+
+    def pbs_rollout_f32(self, nx, ny, cloth, x, v, steps, k0=0):
+        x = np.ascontiguousarray(x, np.float32).copy()
+        v = np.ascontiguousarray(v, np.float32).copy()
+        self._ck(self.lib.ref_pbs_rollout_f32(nx, ny, C.byref(cloth), _p(x), _p(v), steps, k0))
+        return x, v
+
+    def benchmark_sim(self, nx, ny, cloth, x0, v0, steps, warmup, f64=False, threads=1):
+        sec = C.c_double()
+        self._ck(self.lib.ref_benchmark_sim(nx, ny, C.byref(cloth), _p(x0), _p(v0), steps, warmup,
+                                            int(f64), threads, C.byref(sec)))
+        return sec.value
 
     def benchmark_net(self, nx, ny, cloth, params, x0, v0, steps, warmup, f64=False, threads=1):
         sec = C.c_double()

@@ -59,7 +59,8 @@ NetworkParams to_params(const sc_params* p) {
 // A reference Scene for one cloth descriptor. Initial state: the given positions/velocities
 // (double), else the flat build_grid sheet.
 Scene to_scene(int nx, int ny, const sc_cloth_desc* cd, const double* x0, const double* v0) {
-  GridInit g = build_grid(nx, ny, 1.0 / (nx - 1), Vec3{}, GridPlane::XY);
+  GridInit g = build_grid(nx, ny, cd->spacing > 0.0 ? cd->spacing : 1.0 / (nx - 1), Vec3{},
+                          GridPlane::XY);
   Scene s;
   s.name = "harness";
   s.topology = std::move(g.topology);
@@ -69,6 +70,8 @@ Scene to_scene(int nx, int ny, const sc_cloth_desc* cd, const double* x0, const 
     for (size_t i = 0; i < n; ++i) s.initial.x[i] = {x0[3 * i], x0[3 * i + 1], x0[3 * i + 2]};
   if (v0)
     for (size_t i = 0; i < n; ++i) s.initial.v[i] = {v0[3 * i], v0[3 * i + 1], v0[3 * i + 2]};
+  s.material.stiffness = cd->stiffness;
+  s.material.damping = cd->damping;
   s.material.mass = cd->mass;
   s.material.drag = cd->drag;
   s.material.pressure = cd->pressure;
@@ -277,6 +280,84 @@ int ref_rollout_f64(int nx, int ny, const sc_cloth_desc* cd, const sc_params* p,
       copy_out(frames_x + 3 * n * f, t.frames[static_cast<size_t>(f)].x);
       copy_out(frames_v + 3 * n * f, t.frames[static_cast<size_t>(f)].v);
     }
+  });
+}
+
+// ---- the ground-truth mass-spring step (PBS) --------------------------------------------
+
+int ref_total_impulse_f64(int nx, int ny, const sc_cloth_desc* cd, const double* x,
+                          const double* v, double* out) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, nullptr, nullptr);
+    ClothState s;
+    copy_in(s.x, x, static_cast<size_t>(nx) * ny);
+    copy_in(s.v, v, static_cast<size_t>(nx) * ny);
+    copy_out(out, total_impulse(s, scene));
+  });
+}
+
+int ref_pbs_step_f64(int nx, int ny, const sc_cloth_desc* cd, const double* x, const double* v,
+                     double t_next, double* xo, double* vo) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, nullptr, nullptr);
+    ClothState s;
+    copy_in(s.x, x, static_cast<size_t>(nx) * ny);
+    copy_in(s.v, v, static_cast<size_t>(nx) * ny);
+    const ClothState out = step_semi_implicit(s, scene, t_next);
+    copy_out(xo, out.x);
+    copy_out(vo, out.v);
+  });
+}
+
+// simulate_scene (sim.cpp:157-175): frames [(steps+1)][n][3].
+int ref_simulate_f64(int nx, int ny, const sc_cloth_desc* cd, const double* x0, const double* v0,
+                     int steps, double* frames_x, double* frames_v) {
+  return guarded([&] {
+    Scene scene = to_scene(nx, ny, cd, x0, v0);
+    scene.steps = steps;
+    const Trajectory t = simulate_scene(scene);
+    const size_t n = static_cast<size_t>(nx) * ny;
+    for (int f = 0; f < t.frame_count(); ++f) {
+      copy_out(frames_x + 3 * n * f, t.frames[static_cast<size_t>(f)].x);
+      copy_out(frames_v + 3 * n * f, t.frames[static_cast<size_t>(f)].v);
+    }
+  });
+}
+
+// run_steps<float> with params == nullptr (eval.cpp:53-55): the benchmark_sim sequence.
+int ref_pbs_rollout_f32(int nx, int ny, const sc_cloth_desc* cd, float* x, float* v, int steps,
+                        int k0) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, nullptr, nullptr);
+    const auto kernel = detail::make_scene_kernel<float>(scene);
+    const size_t n = static_cast<size_t>(nx) * ny;
+    std::vector<Vec3f> xs, vs, xn(n), vn(n), imp(n);
+    copy_in(xs, x, n);
+    copy_in(vs, v, n);
+    for (int k = k0; k < k0 + steps; ++k) {
+      detail::total_impulse(xs.data(), vs.data(), kernel, imp.data());
+      detail::advance_with_impulse(xs.data(), vs.data(), imp.data(), kernel,
+                                   static_cast<float>(k + 1) * kernel.dt, xn.data(), vn.data(),
+                                   nullptr);
+      xs.swap(xn);
+      vs.swap(vn);
+    }
+    copy_out(x, xs);
+    copy_out(v, vs);
+  });
+}
+
+int ref_benchmark_sim(int nx, int ny, const sc_cloth_desc* cd, const double* x0,
+                      const double* v0, int steps, int warmup, int f64, int threads,
+                      double* seconds) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, x0, v0);
+    const int before = thread_count();
+    set_thread_count(threads);
+    const BenchResult r =
+        benchmark_sim(scene, steps, warmup, f64 ? Precision::F64 : Precision::F32);
+    set_thread_count(before);
+    *seconds = r.seconds;
   });
 }
 

@@ -15,8 +15,8 @@ from .scene import (BoundarySpec, ConfigError, GridPlane, IoError, MaterialParam
                     SphereCollider, Trajectory, build_grid, channel_order_hash, load_scene,
                     params_fingerprint, parse_scene)
 from .api import (BenchResult, ClothBatch, Context, CudaError, advance_with_impulse,  # noqa: E402
-                  apply_dirichlet, benchmark_net, forward_impulse, nn_step, plug_impulse,
-                  rollout)
+                  apply_dirichlet, benchmark_net, benchmark_sim, forward_impulse, nn_step,
+                  plug_impulse, rollout, simulate, step_semi_implicit, total_impulse)
 
 __all__ = [
     "BenchResult", "BoundarySpec", "ClothBatch", "ConfigError", "Context", "CudaError",
@@ -24,5 +24,6 @@ __all__ = [
     "PlaneCollider", "PlugForce", "Scene", "SphereCollider", "Trajectory", "advance_with_impulse",
     "apply_dirichlet", "benchmark_net", "build_grid", "channel_order_hash", "forward_impulse",
     "load_scene", "nn_step", "params_fingerprint", "parse_scene", "plug_impulse", "rollout",
+    "benchmark_sim", "simulate", "step_semi_implicit", "total_impulse",
 ]
 __version__ = "0.1.0"

@@ -56,6 +56,9 @@ class sc_cloth_desc(C.Structure):
         ("spheres", C.POINTER(sc_sphere)),
         ("n_planes", C.c_int32),
         ("planes", C.POINTER(sc_plane)),
+        ("stiffness", C.c_double),
+        ("damping", C.c_double),
+        ("spacing", C.c_double),
     ]
 
 
@@ -92,6 +95,10 @@ SIGNATURES = {
     "sc_advance_with_impulse": (C.c_int, [_P, _P, _P, _P, C.c_double, _P, _P, _P]),
     "sc_nn_step": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, _P, _P, _P]),
     "sc_benchmark": (C.c_int, [_P, _I, _I, C.c_int, C.POINTER(C.c_double)]),
+    "sc_total_impulse": (C.c_int, [_P, _P, _P, _P]),
+    "sc_pbs_step": (C.c_int, [_P, _P, _P, C.c_double, _P, _P, _P]),
+    "sc_simulate_frames": (C.c_int, [_P, _P, _P, _I, _I, _P, _P]),
+    "sc_benchmark_sim": (C.c_int, [_P, _I, _I, C.POINTER(C.c_double)]),
     "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),
     "sc_ctx_halo_elems": (C.c_int64, [_P]),

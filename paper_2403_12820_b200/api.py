@@ -194,6 +194,35 @@ class Context:
                                              MODES[mode], _ptr(xo), _ptr(vo), _ptr(m)))
         return (xo, vo, m) if constrained else (xo, vo)
 
+    # -- ground-truth mass-spring step (PBS) --
+    def total_impulse(self, x, v) -> np.ndarray:
+        x, v = self._arr(x), self._arr(v)
+        out = self._empty()
+        _raise(self.lib, self.lib.sc_total_impulse(self.h, _ptr(x), _ptr(v), _ptr(out)))
+        return out
+
+    def pbs_step(self, x, v, t_next: float, constrained: bool = False):
+        x, v = self._arr(x), self._arr(v)
+        xo, vo = self._empty(), self._empty()
+        m = np.zeros((self.batch, self.nx * self.ny), np.uint8) if constrained else None
+        _raise(self.lib, self.lib.sc_pbs_step(self.h, _ptr(x), _ptr(v), float(t_next), _ptr(xo),
+                                              _ptr(vo), _ptr(m)))
+        return (xo, vo, m) if constrained else (xo, vo)
+
+    def simulate_frames(self, x0, v0, steps: int, stride: int = 1):
+        x0, v0 = self._arr(x0), self._arr(v0)
+        nf = steps // stride + 1
+        fx = np.empty((nf,) + (self.batch, self.local_rows * self.nx, 3), self.dtype)
+        fv = np.empty_like(fx)
+        _raise(self.lib, self.lib.sc_simulate_frames(self.h, _ptr(x0), _ptr(v0), int(steps),
+                                                     int(stride), _ptr(fx), _ptr(fv)))
+        return fx, fv
+
+    def benchmark_sim(self, steps: int, warmup: int) -> float:
+        sec = C.c_double()
+        _raise(self.lib, self.lib.sc_benchmark_sim(self.h, int(steps), int(warmup), C.byref(sec)))
+        return sec.value
+
     def benchmark(self, steps: int, warmup: int, mode: str = "parity") -> float:
         sec = C.c_double()
         _raise(self.lib, self.lib.sc_benchmark(self.h, int(steps), int(warmup), MODES[mode],
@@ -380,6 +409,102 @@ def benchmark_net(params: NetworkParams, scene: Scene, steps: int, warmup: int,
     with Context(scene, params, precision, device) as ctx:
         ctx.set_state(scene.initial_x, scene.initial_v)
         sec = ctx.benchmark(steps, warmup, mode)
+    return BenchResult(steps, warmup, precision, sec, steps / max(sec, 1e-12))
+
+
+# ---------------------------------------------- ground-truth mass-spring step (PBS, §8 f2) ----
+
+def _force_terms(x: np.ndarray, v: np.ndarray, scene: Scene):
+    """The four force terms of total_force (sim.cpp:77-88) in float64, vectorised; used only on
+    the failure path to name the term that went non-finite (diagnose_divergence, sim.cpp:23-48)."""
+    nx, ny = scene.nx, scene.ny
+    m = scene.material
+    X = x.reshape(ny, nx, 3)
+    Vv = v.reshape(ny, nx, 3)
+    el = np.zeros_like(X)
+    da = np.zeros_like(X)
+    with np.errstate(all="ignore"):
+        for dx, dy, mult in STENCIL_OFFSETS:
+            rest = scene.spacing * mult
+            ys = slice(max(0, -dy), ny - max(0, dy))
+            xs = slice(max(0, -dx), nx - max(0, dx))
+            yj = slice(max(0, dy), ny + min(0, dy))
+            xj = slice(max(0, dx), nx + min(0, dx))
+            d = X[ys, xs] - X[yj, xj]
+            ln = np.sqrt((d * d).sum(-1, keepdims=True))
+            el[ys, xs] -= d * (m.stiffness * (ln - rest) / ln)
+            dr = d / ln
+            da[ys, xs] -= dr * (m.damping * ((Vv[ys, xs] - Vv[yj, xj]) * dr).sum(-1, keepdims=True))
+        pr = np.zeros_like(X)
+        if m.pressure != 0.0:
+            c = X[1:-1, 1:-1]
+            e, n = c - X[1:-1, 2:], c - X[2:, 1:-1]
+            w, s = c - X[1:-1, :-2], c - X[:-2, 1:-1]
+            pr[1:-1, 1:-1] = (np.cross(e, n) + np.cross(n, w) + np.cross(w, s) + np.cross(s, e)) * m.pressure
+        ex = m.gravity * m.mass - Vv * m.drag
+    return [(name, t.reshape(-1, 3)) for name, t in
+            (("elastic", el), ("damping", da), ("pressure", pr), ("external", ex))]
+
+
+def _diagnose_divergence(x, v, scene: Scene) -> str:
+    for name, f in _force_terms(x, v, scene):
+        bad = np.where(~np.isfinite(f).all(axis=1))[0]
+        if len(bad):
+            return "%s force non-finite at node %d (reduce dt or stiffness)" % (name, bad[0])
+    return "non-finite state update (reduce dt or stiffness)"
+
+
+def total_impulse(scene: Scene, positions, velocities, device: int = 0) -> np.ndarray:
+    """Total force scaled by dt/m (sim.cpp:90-98), float64, bit-identical to the reference."""
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    with Context(scene, None, "f64", device) as ctx:
+        return ctx.total_impulse(x, v)[0]
+
+
+def step_semi_implicit(scene: Scene, positions, velocities, t_next: float, device: int = 0):
+    """One ground-truth step to the frame at t_next (sim.cpp:150-155); returns (x, v)."""
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    with Context(scene, None, "f64", device) as ctx:
+        try:
+            xo, vo = ctx.pbs_step(x, v, t_next)
+        except NumericsError as e:
+            if "singular" in str(e):
+                raise
+            raise NumericsError(_diagnose_divergence(x, v, scene)) from None
+    return xo[0], vo[0]
+
+
+def simulate(scene: Scene, device: int = 0) -> Trajectory:
+    """simulate_scene (sim.cpp:157-175): scene.steps ground-truth steps from the pinned initial
+    state, every frame stored; bit-identical to the reference, including its error text."""
+    scene.validate()
+    x0, v0 = apply_dirichlet(scene.initial_x, scene.initial_v, scene, 0.0)
+    with Context(scene, None, "f64", device) as ctx:
+        fx, fv = ctx.simulate_frames(x0, v0, scene.steps, 1)
+        fs, fn, fstate = ctx.health()
+    sing, state = int(fs[0]), int(fstate[0])
+    if sing >= 0 and (state < 0 or sing <= state):
+        raise NumericsError("simulation diverged at frame %d: elastic force: singular spring "
+                            "(coincident nodes) at node %d" % (sing, int(fn[0])))
+    if state >= 0:
+        raise NumericsError("simulation diverged at frame %d: %s" % (
+            state, _diagnose_divergence(fx[state - 1, 0], fv[state - 1, 0], scene)))
+    return Trajectory(scene.nx, scene.ny, scene.dt, scene.spacing, fx[:, 0], fv[:, 0])
+
+
+def benchmark_sim(scene: Scene, steps: int, warmup: int, precision: str = "f32",
+                  device: int = 0) -> BenchResult:
+    """Device-timed ground-truth stepping (benchmark_sim, eval.cpp:151-153)."""
+    scene.validate()
+    if steps < 1:
+        raise ConfigError("bench: steps must be >= 1")
+    if warmup < 0:
+        raise ConfigError("bench: warmup must be >= 0")
+    with Context(scene, None, precision, device) as ctx:
+        ctx.set_state(scene.initial_x, scene.initial_v)
+        sec = ctx.benchmark_sim(steps, warmup)
     return BenchResult(steps, warmup, precision, sec, steps / max(sec, 1e-12))
 
 

@@ -130,6 +130,7 @@ struct sc_ctx {
   FastPlan plan_gen{};   // general finish
   std::map<long long, FastPlan> plan_cache;  // row-range launches of strip contexts
   bool any_pressure = false, any_general = false;
+  bool pbs_ok = false;  // every cloth has a grid spacing (rest lengths) for the PBS step
   CUtensorMap tmap[2][2];  // [buffer][xy pairs | z planes]
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
@@ -185,6 +186,12 @@ void validate_scene(const sc_scene_desc* s) {
     if (!std::isfinite(c.drag) || c.drag < 0.0)
       throw_config(at + "material.drag: must be a finite value >= 0");
     if (!std::isfinite(c.pressure)) throw_config(at + "material.pressure: must be finite");
+    if (!std::isfinite(c.stiffness) || c.stiffness < 0.0)
+      throw_config(at + "material.stiffness: must be a finite value >= 0");
+    if (!std::isfinite(c.damping) || c.damping < 0.0)
+      throw_config(at + "material.damping: must be a finite value >= 0");
+    if (!std::isfinite(c.spacing) || c.spacing < 0.0)
+      throw_config(at + "grid.spacing: must be a finite value > 0");
     if (!finite3(c.gravity)) throw_config(at + "material.gravity: components must be finite");
     if (!(c.dt > 0.0) || !std::isfinite(c.dt))
       throw_config(at + "time.dt: must be a finite value > 0");
@@ -282,6 +289,17 @@ void upload_scene(sc_ctx* c, const sc_scene_desc* s) {
       pc.omf = T(1) - static_cast<T>(d.planes[q].friction);
       pln.push_back(pc);
     }
+    // PBS material (SceneKernel<T> casts, kernels.hpp:62-70; rest lengths grid.cpp:93-95)
+    k.stiffness = static_cast<T>(d.stiffness);
+    k.damping = static_cast<T>(d.damping);
+    k.mass = mass;
+    k.drag = static_cast<T>(d.drag);
+    for (int q = 0; q < 3; ++q) k.grav[q] = static_cast<T>(d.gravity[q]);
+    static const double mult[kChannels] = {1.0, 1.0, 1.0, 1.0,
+                                           1.41421356237309504880, 1.41421356237309504880,
+                                           1.41421356237309504880, 1.41421356237309504880,
+                                           2.0, 2.0, 2.0, 2.0};
+    for (int c = 0; c < kChannels; ++c) k.rest[c] = static_cast<T>(d.spacing * mult[c]);
     k.n_pins = d.n_pins;
     k.pin_row_lo = d.n_pins > 0 ? d.pin_nodes[0] / s->nx : 0;  // pins are sorted
     k.pin_row_hi = d.n_pins > 0 ? d.pin_nodes[d.n_pins - 1] / s->nx : -1;
@@ -511,14 +529,16 @@ void download_state(sc_ctx* c, int which, void* x, void* v, bool sync = true) {
   if (sync) ck(cudaStreamSynchronize(c->stream), "D2H sync");
 }
 
-void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last) {
+void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last,
+                  int kind = KIND_STEP) {
   if (steps < 0) throw_config("steps: must be >= 0");
   if (mode != SC_MODE_PARITY && mode != SC_MODE_FAST) throw_config("mode: unknown");
   if (mode == SC_MODE_FAST && c->prec != SC_F32)
     throw_config("mode: FAST is an f32 mode (use PARITY with an f64 context)");
   int s = 0;
   // FAST: the persistent multi-step kernel for all but a mask-producing last step
-  const int multi = (mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok && c->multi_on &&
+  const int multi = (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok &&
+                     c->multi_on &&
                      c->plan.multi_ok)
                         ? steps - (dev_mask_last ? 1 : 0)
                         : 0;
@@ -539,10 +559,10 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
     const int k = k0 + s;
     uint8_t* m = (s == steps - 1) ? dev_mask_last : nullptr;
     if (c->prec == SC_F32)
-      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr,
+      launch_one<float>(c, kind, mode, k, false, 0.0, m, nullptr,
                         c->health_on ? c->health.p : nullptr, c->u0, c->u1, c->stream);
     else
-      launch_one<double>(c, KIND_STEP, mode, k, false, 0.0, m, nullptr,
+      launch_one<double>(c, kind, mode, k, false, 0.0, m, nullptr,
                          c->health_on ? c->health.p : nullptr, c->u0, c->u1, c->stream);
     c->cur = 1 - c->cur;
   }
@@ -643,6 +663,8 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
     c->health.ensure(static_cast<size_t>(c->batch));
     reset_health(c);
     c->any_pressure = c->any_general = false;
+    c->pbs_ok = true;
+    for (int b = 0; b < s->batch; ++b) c->pbs_ok = c->pbs_ok && s->cloths[b].spacing > 0.0;
     for (int b = 0; b < s->batch; ++b) {
       const sc_cloth_desc& d = s->cloths[b];
       const bool pres = d.plug_pressure && static_cast<float>(d.pressure) != 0.0f;
@@ -814,7 +836,7 @@ void op_call(sc_ctx* c, int kind, sc_mode mode, const void* x, const void* v,
   launch_one<T>(c, kind, mode, 0, true, t_next, dm, dimp, c->health.p, c->u0, c->u1, c->stream);
   if (impulse_out)
     ck(cudaMemcpyAsync(impulse_out, dimp, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H imp");
-  if (kind == KIND_STEP || kind == KIND_ADVANCE) {
+  if (kind == KIND_STEP || kind == KIND_ADVANCE || kind == KIND_PBS) {
     download_state(c, 1 - c->cur, xo, vo, false);
     if (constrained)
       ck(cudaMemcpyAsync(constrained, dm, static_cast<size_t>(c->batch) * c->nodes_global(),
@@ -822,6 +844,24 @@ void op_call(sc_ctx* c, int kind, sc_mode mode, const void* x, const void* v,
          "D2H mask");
   }
   ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+// NumericsError of the PBS step: a singular spring (kernels.hpp:105-107, batch 1 node index),
+// then a non-finite state (sim.cpp:153 -> diagnose_divergence; the force term is named by the
+// Python layer, which can evaluate the terms separately).
+void pbs_check(sc_ctx* c, bool state) {
+  std::vector<Health> h(static_cast<size_t>(c->batch));
+  ck(cudaMemcpy(h.data(), c->health.p, sizeof(Health) * h.size(), cudaMemcpyDeviceToHost),
+     "D2H health");
+  for (int b = 0; b < c->batch; ++b)
+    if (h[static_cast<size_t>(b)].impulse_key != ~0ull)
+      throw Fail{SC_ERR_NUMERICS, "elastic force: singular spring (coincident nodes) at node " +
+                                      std::to_string(h[static_cast<size_t>(b)].impulse_key &
+                                                     0xffffffffu)};
+  if (state)
+    for (int b = 0; b < c->batch; ++b)
+      if (h[static_cast<size_t>(b)].state_frame != INT_MAX)
+        throw Fail{SC_ERR_NUMERICS, "non-finite state update (reduce dt or stiffness)"};
 }
 
 sc_status op_entry(sc_ctx* c, int kind, sc_mode mode, const void* x, const void* v,
@@ -834,10 +874,13 @@ sc_status op_entry(sc_ctx* c, int kind, sc_mode mode, const void* x, const void*
     if (mode == SC_MODE_FAST && c->prec != SC_F32) throw_config("mode: FAST is an f32 mode");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_health(c);
+    if ((kind == KIND_PBS || kind == KIND_TOTAL) && !c->pbs_ok)
+      throw_config("grid.spacing: must be a finite value > 0 (rest lengths of the PBS step)");
     if (c->prec == SC_F32)
       op_call<float>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
     else
       op_call<double>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
+    if (kind == KIND_PBS || kind == KIND_TOTAL) pbs_check(c, kind == KIND_PBS);
   });
 }
 }  // namespace
@@ -879,6 +922,75 @@ sc_status sc_nn_step(sc_ctx* c, const void* x, const void* v, double t_next, sc_
     return SC_ERR_CONFIG;
   }
   return op_entry(c, KIND_STEP, mode, x, v, nullptr, nullptr, t_next, xo, vo, constrained, true);
+}
+
+sc_status sc_total_impulse(sc_ctx* c, const void* x, const void* v, void* impulse) {
+  if (!impulse) {
+    g_err = "impulse: null array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_TOTAL, SC_MODE_PARITY, x, v, nullptr, impulse, 0.0, nullptr, nullptr,
+                  nullptr, false);
+}
+
+sc_status sc_pbs_step(sc_ctx* c, const void* x, const void* v, double t_next, void* xo, void* vo,
+                      uint8_t* constrained) {
+  if (!xo || !vo) {
+    g_err = "pbs_step: null output array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_PBS, SC_MODE_PARITY, x, v, nullptr, nullptr, t_next, xo, vo,
+                  constrained, false);
+}
+
+sc_status sc_simulate_frames(sc_ctx* c, const void* x0, const void* v0, int32_t steps,
+                             int32_t stride, void* fx, void* fv) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (!c->pbs_ok)
+      throw_config("grid.spacing: must be a finite value > 0 (rest lengths of the PBS step)");
+    if (stride < 1) throw_config("stride: must be >= 1");
+    if (!x0 || !v0 || !fx || !fv) throw_config("frames: null array");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const bool health_before = c->health_on;
+    c->health_on = true;  // simulate_scene checks every step (sim.cpp:153)
+    reset_health(c);
+    upload_state(c, x0, v0);
+    const size_t frame_bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
+    std::memcpy(fx, x0, frame_bytes);
+    std::memcpy(fv, v0, frame_bytes);
+    int f = 1;
+    for (int k = 0; k < steps; k += stride) {
+      const int n = std::min(stride, steps - k);
+      advance_impl(c, n, k, SC_MODE_PARITY, nullptr, KIND_PBS);
+      if (n == stride) {
+        download_state(c, c->cur, static_cast<unsigned char*>(fx) + frame_bytes * f,
+                       static_cast<unsigned char*>(fv) + frame_bytes * f);
+        ++f;
+      }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->health_on = health_before;
+  });
+}
+
+sc_status sc_benchmark_sim(sc_ctx* c, int32_t steps, int32_t warmup, double* seconds) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (!c->pbs_ok)
+      throw_config("grid.spacing: must be a finite value > 0 (rest lengths of the PBS step)");
+    if (steps < 1) throw_config("bench: steps must be >= 1");
+    if (warmup < 0) throw_config("bench: warmup must be >= 0");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    advance_impl(c, warmup, 0, SC_MODE_PARITY, nullptr, KIND_PBS);
+    ck(cudaEventRecord(c->ev0, c->stream), "event");
+    advance_impl(c, steps, warmup, SC_MODE_PARITY, nullptr, KIND_PBS);
+    ck(cudaEventRecord(c->ev1, c->stream), "event");
+    ck(cudaEventSynchronize(c->ev1), "event sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
+    if (seconds) *seconds = ms * 1e-3;
+  });
 }
 
 sc_status sc_benchmark(sc_ctx* c, int32_t steps, int32_t warmup, sc_mode mode, double* seconds) {

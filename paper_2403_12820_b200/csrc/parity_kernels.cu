@@ -6,6 +6,9 @@
 //   KIND_FORWARD forward_impulse only                    (kernels.hpp:265-282)
 //   KIND_PLUG    add_plug_impulse on a zero field        (sim.cpp:100-106)
 //   KIND_ADVANCE advance_with_impulse with a given field (kernels.hpp:205-252)
+//   KIND_PBS     total_impulse -> advance_with_impulse: step_semi_implicit (sim.cpp:150-155),
+//                the ground-truth mass-spring step
+//   KIND_TOTAL   total_impulse only (kernels.hpp:165-175)
 // Every floating-point operation is a non-contractible IEEE RN primitive in the reference's
 // order; this TU is additionally compiled with --fmad=false.
 //
@@ -99,6 +102,81 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
             (static_cast<unsigned long long>(a.k + 1) << 32) | static_cast<unsigned long long>(gnode);
         atomicMin(&a.health[b].impulse_key, key);
       }
+    } else if (KIND == KIND_PBS || KIND == KIND_TOTAL) {
+      // total_impulse<T> (kernels.hpp:165-175): elastic, damping, pressure, external, * dt/m
+      T f[3] = {T(0), T(0), T(0)};
+      bool singular = false;
+#pragma unroll
+      for (int c = 0; c < kChannels; ++c) {  // accumulate_elastic (kernels.hpp:86-108)
+        const int jx = ix + off_dx(c), jy = iy + off_dy(c);
+        if (jx < 0 || jx >= a.nx || jy < 0 || jy >= a.ny) continue;
+        T dd[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dd[d] = R::sub(x[d], S(d, ly + off_dy(c), lx + off_dx(c)));
+        const T len =
+            R::sqrt(R::add(R::add(R::mul(dd[0], dd[0]), R::mul(dd[1], dd[1])), R::mul(dd[2], dd[2])));
+        if (len == T(0)) {
+          singular = true;
+          continue;
+        }
+        const T sc = R::div(R::mul(cc.stiffness, R::sub(len, cc.rest[c])), len);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) f[d] = R::sub(f[d], R::mul(dd[d], sc));
+      }
+#pragma unroll
+      for (int c = 0; c < kChannels; ++c) {  // accumulate_damping (kernels.hpp:112-136)
+        const int jx = ix + off_dx(c), jy = iy + off_dy(c);
+        if (jx < 0 || jx >= a.nx || jy < 0 || jy >= a.ny) continue;
+        T dd[3], dv[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          dd[d] = R::sub(x[d], S(d, ly + off_dy(c), lx + off_dx(c)));
+          dv[d] = R::sub(v[d], S(3 + d, ly + off_dy(c), lx + off_dx(c)));
+        }
+        const T len =
+            R::sqrt(R::add(R::add(R::mul(dd[0], dd[0]), R::mul(dd[1], dd[1])), R::mul(dd[2], dd[2])));
+        if (len == T(0)) continue;
+        T dir[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dir[d] = R::div(dd[d], len);
+        const T sc = R::mul(cc.damping, R::add(R::add(R::mul(dv[0], dir[0]), R::mul(dv[1], dir[1])),
+                                               R::mul(dv[2], dir[2])));
+#pragma unroll
+        for (int d = 0; d < 3; ++d) f[d] = R::sub(f[d], R::mul(dir[d], sc));
+      }
+      if (cc.pressure != T(0) && ix >= 1 && ix <= a.nx - 2 && iy >= 1 && iy <= a.ny - 2) {
+        // accumulate_pressure (kernels.hpp:142-155): interior nodes only, added into f
+        T e[3], n[3], w[3], s[3], c1[3], c2[3], c3[3], c4[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          e[d] = R::sub(x[d], S(d, ly, lx + 1));
+          n[d] = R::sub(x[d], S(d, ly + 1, lx));
+          w[d] = R::sub(x[d], S(d, ly, lx - 1));
+          s[d] = R::sub(x[d], S(d, ly - 1, lx));
+        }
+        auto cross = [](const T* p, const T* q, T* o) {
+          o[0] = R::sub(R::mul(p[1], q[2]), R::mul(p[2], q[1]));
+          o[1] = R::sub(R::mul(p[2], q[0]), R::mul(p[0], q[2]));
+          o[2] = R::sub(R::mul(p[0], q[1]), R::mul(p[1], q[0]));
+        };
+        cross(e, n, c1);
+        cross(n, w, c2);
+        cross(w, s, c3);
+        cross(s, e, c4);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          f[d] = R::add(f[d], R::mul(R::add(R::add(R::add(c1[d], c2[d]), c3[d]), c4[d]), cc.pressure));
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {  // accumulate_external (kernels.hpp:159-162), then * dt/m
+        f[d] = R::add(f[d], R::sub(R::mul(cc.grav[d], cc.mass), R::mul(v[d], cc.drag)));
+        imp[d] = R::mul(f[d], cc.scale);
+      }
+      if (singular && a.health) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(a.k + 1) << 32) | static_cast<unsigned long long>(gnode);
+        atomicMin(&a.health[b].impulse_key, key);
+      }
     } else if (KIND == KIND_PLUG) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) imp[d] = T(0);
@@ -124,7 +202,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
       plug_tail(cc, v, imp);
     }
 
-    if (KIND == KIND_FORWARD || KIND == KIND_PLUG) {
+    if (KIND == KIND_FORWARD || KIND == KIND_PLUG || KIND == KIND_TOTAL) {
       T* op = a.impulse + (static_cast<int64_t>(b) * nodes + gnode) * 3;
 #pragma unroll
       for (int d = 0; d < 3; ++d) op[d] = imp[d];
@@ -172,6 +250,10 @@ cudaError_t launch_parity(const StepArgs<T>& a, int kind, cudaStream_t stream) {
       return launch_parity_t<T, KIND_PLUG>(a, stream);
     case KIND_ADVANCE:
       return launch_parity_t<T, KIND_ADVANCE>(a, stream);
+    case KIND_PBS:
+      return launch_parity_t<T, KIND_PBS>(a, stream);
+    case KIND_TOTAL:
+      return launch_parity_t<T, KIND_TOTAL>(a, stream);
   }
   return cudaErrorInvalidValue;
 }

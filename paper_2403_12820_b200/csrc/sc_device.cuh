@@ -89,6 +89,10 @@ struct ClothConst {
   int32_t n_spheres, sphere0, n_planes, plane0;
   int32_t n_pins;
   int32_t pin_row_lo, pin_row_hi;  // rows holding pins (skip the bitmap lookup elsewhere)
+  // ground-truth mass-spring step (PBS): MaterialParams cast to T (kernels.hpp:62-70)
+  T stiffness, damping, mass, drag;
+  T grav[3];
+  T rest[kChannels];  // topology rest lengths spacing * {1, sqrt2, 2} cast to T (kernels.hpp:69-70)
   int64_t pin_word0;  // first word of this cloth's pin bitmap / rank prefix
   int64_t anchor0;    // first anchor (x3) of this cloth
 };
@@ -110,7 +114,8 @@ struct PlaneConst {
 };
 
 struct Health {
-  // min over (frame << 32 | node) of non-finite cell impulses (net.cpp:139-140); ~0 if none
+  // min over (frame << 32 | node) of non-finite cell impulses (net.cpp:139-140) — for the PBS
+  // step: of singular springs (kernels.hpp:96-107); ~0 if none
   unsigned long long impulse_key;
   int32_t state_frame;  // first frame with a non-finite x' or v' (eval.cpp:98-99); INT_MAX
   int32_t pad;

@@ -352,6 +352,9 @@ class Scene:
         d.spheres = C.cast(sph, C.POINTER(_abi.sc_sphere))
         d.n_planes = len(self.planes)
         d.planes = C.cast(pl, C.POINTER(_abi.sc_plane))
+        d.stiffness = float(self.material.stiffness)
+        d.damping = float(self.material.damping)
+        d.spacing = float(self.spacing)
         return d
 
 

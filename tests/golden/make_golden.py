@@ -151,5 +151,40 @@ def main():
          frames_x=fx, frames_v=fv)
 
 
+def pbs_main():
+    """Ground-truth mass-spring step (PBS) fixtures from the reference."""
+    rng = np.random.default_rng(20240320)
+    # f64 simulate_scene: a sheet dropped on a sphere with friction, a moving pin, pressure,
+    # drag (like acceptance criterion 6's ball scene, smaller)
+    nx, ny = 12, 10
+    sp = 0.05
+    x0 = sheet(rng, nx, ny, sp, 1e-3, origin=(-0.275, -0.225, 0.28))
+    v0 = np.zeros_like(x0)
+    pins = [0, nx - 1]
+    sc = scene_arrays(nx, ny, 4e-4, mass=0.01, drag=0.01, pressure=0.7, gravity=(0.0, 0.0, -9.8),
+                      plugs=(0, 0, 0), pin_nodes=pins, pin_anchors=x0[pins],
+                      pin_velocity=(0.02, 0.0, 0.0), spheres=[(0.0, 0.0, 0.0, 0.25, 0.3)],
+                      stiffness=40.0, damping=0.2, spacing=sp)
+    keep = []
+    cd = cloth_desc(sc, keep)
+    fx, fv = R.simulate_f64(nx, ny, cd, x0, v0, 150)
+    xs, vs = fx[60].copy(), fv[60].copy()
+    imp = R.total_impulse_f64(nx, ny, cd, xs, vs)
+    save("pbs_sim64", **sc, x0=x0, v0=v0, frames_x=fx, frames_v=fv, imp60=imp)
+    # f32: the benchmark_sim step sequence (run_steps<float>, params == nullptr)
+    x32 = x0.astype(np.float32)
+    v32 = np.zeros_like(x32)
+    outs = {}
+    xk, vk = x32, v32
+    k = 0
+    for cp in (1, 20, 100):
+        xk, vk = R.pbs_rollout_f32(nx, ny, cd, xk, vk, cp - k, k)
+        k = cp
+        outs["x_%d" % cp], outs["v_%d" % cp] = xk.copy(), vk.copy()
+    save("pbs_steps32", **sc, x0=x32, v0=v32, checkpoints=np.array([1, 20, 100]), **outs)
+
+
 if __name__ == "__main__":
-    main()
+    if "--pbs" not in sys.argv:
+        main()
+    pbs_main()

@@ -17,8 +17,10 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def scene_arrays(nx, ny, dt, mass=1.0, drag=0.0, pressure=0.0, gravity=(0, 0, -9.8),
                  plugs=(0, 1, 0), pin_nodes=(), pin_anchors=None, pin_velocity=(0, 0, 0),
-                 spheres=(), planes=()):
+                 spheres=(), planes=(), stiffness=0.0, damping=0.0, spacing=None):
     return dict(
+        stiffness=np.float64(stiffness), damping=np.float64(damping),
+        spacing=np.float64(spacing if spacing is not None else 1.0 / (nx - 1)),
         nx=np.int64(nx), ny=np.int64(ny), dt=np.float64(dt), mass=np.float64(mass),
         drag=np.float64(drag), pressure=np.float64(pressure),
         gravity=np.asarray(gravity, np.float64), plugs=np.asarray(plugs, np.int64),
@@ -60,6 +62,11 @@ def cloth_desc(z, keep: list, prefix: str = "") -> _abi.sc_cloth_desc:
     d.spheres = C.cast(sph, C.POINTER(_abi.sc_sphere))
     d.n_planes = len(pl_a)
     d.planes = C.cast(pl, C.POINTER(_abi.sc_plane))
+    # fixtures written before the PBS fields existed default to no springs
+    d.stiffness = float(z[prefix + "stiffness"]) if prefix + "stiffness" in z else 0.0
+    d.damping = float(z[prefix + "damping"]) if prefix + "damping" in z else 0.0
+    nx = int(z[prefix + "nx"])
+    d.spacing = float(z[prefix + "spacing"]) if prefix + "spacing" in z else 1.0 / (nx - 1)
     return d
 
 
@@ -83,8 +90,11 @@ def to_scene(z, x0=None):
     from paper_2403_12820_b200 import PlaneCollider, PlugForce, Scene, SphereCollider
 
     nx, ny = int(z["nx"]), int(z["ny"])
-    s = Scene(nx, ny, 1.0 / (nx - 1), x0)
+    s = Scene(nx, ny, float(z["spacing"]) if "spacing" in z else 1.0 / (nx - 1), x0)
     s.dt = float(z["dt"])
+    if "stiffness" in z:
+        s.material.stiffness = float(z["stiffness"])
+        s.material.damping = float(z["damping"])
     s.material.mass = float(z["mass"])
     s.material.drag = float(z["drag"])
     s.material.pressure = float(z["pressure"])

@@ -33,7 +33,8 @@ def test_library_exports_every_declared_symbol():
     lib = _abi.load()
     missing = [n for n in sorted(declared_functions()) if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.sc_abi_version() == 1
+    hdr = open(os.path.join(ROOT, "include", "stencilcloth_b200.h")).read()
+    assert lib.sc_abi_version() == int(re.search(r"#define SC_ABI_VERSION (\d+)", hdr).group(1))
 
 
 def test_ctypes_mirror_covers_every_declared_function():

@@ -100,3 +100,40 @@ def test_golden_fixtures_exercise_contacts():
     z = load("sphere_drop_f32")
     per_step = z["masks"].sum(axis=1)
     assert per_step.max() > 50 and per_step[0] == len(z["pin_nodes"])
+
+
+def test_oracle_pbs_matches_reference_bitwise(oracle):
+    """Ground-truth mass-spring step (PBS, §8(f2)): the oracle's total_impulse and
+    step_semi_implicit reproduce simulate_scene's frames (f64) and the benchmark_sim step
+    sequence (f32) bit for bit."""
+    z = load("pbs_sim64")
+    nx, ny = int(z["nx"]), int(z["ny"])
+    keep = []
+    cd = cloth_desc(z, keep)
+    fx, fv = z["frames_x"], z["frames_v"]
+    imp, sing = oracle.total_impulse(nx, ny, cd, fx[60], fv[60])
+    assert sing == -1 and bits_equal(imp, z["imp60"])
+    x, v = fx[0].copy(), fv[0].copy()
+    for k in range(fx.shape[0] - 1):
+        x, v, _, _ = oracle.pbs_step(nx, ny, cd, x, v, (k + 1) * float(z["dt"]))
+        assert bits_equal(x, fx[k + 1]) and bits_equal(v, fv[k + 1]), "frame %d" % (k + 1)
+    z = load("pbs_steps32")
+    cd = cloth_desc(z, keep)
+    x, v = z["x0"].copy(), z["v0"].copy()
+    k = 0
+    for cp in z["checkpoints"]:
+        while k < cp:
+            x, v, _, _ = oracle.pbs_step(nx, ny, cd, x, v, np.float32(k + 1) * np.float32(float(z["dt"])))
+            k += 1
+        assert bits_equal(x, z["x_%d" % cp]) and bits_equal(v, z["v_%d" % cp])
+
+
+def test_oracle_pbs_singular_spring(oracle):
+    z = load("pbs_sim64")
+    nx, ny = int(z["nx"]), int(z["ny"])
+    keep = []
+    cd = cloth_desc(z, keep)
+    x = z["frames_x"][0].copy()
+    x[17] = x[18]  # coincident E neighbours
+    _, sing = oracle.total_impulse(nx, ny, cd, x, z["frames_v"][0])
+    assert sing == 17
