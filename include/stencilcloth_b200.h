@@ -194,6 +194,14 @@ sc_status sc_pbs_step(sc_ctx* ctx, const void* x, const void* v, double t_next, 
  * the first singular spring (impulse frame / node). */
 sc_status sc_simulate_frames(sc_ctx* ctx, const void* x0, const void* v0, int32_t steps,
                              int32_t stride, void* frames_x, void* frames_v);
+/* ---- evaluate_rollout (§8(f4), eval.cpp:105-133) ---------------------------------------- */
+/* Per-frame sums over nodes of |x_test - x_ref| (double AoS [frames][nodes][3] host arrays);
+ * the caller forms 100 * sum / (nodes * bbox diagonal of reference frame 0) like the reference.
+ * Context-free (its own stream on `device`); errors via sc_eval_last_error(). */
+sc_status sc_evaluate_frames(int device, const double* test_x, const double* ref_x,
+                             int32_t frames, int64_t nodes, double* frame_sums);
+const char* sc_eval_last_error(void);
+
 /* benchmark_sim (eval.hpp:46 / eval.cpp:151-153): device-timed PBS steps from the ctx state. */
 sc_status sc_benchmark_sim(sc_ctx* ctx, int32_t steps, int32_t warmup, double* seconds);
 

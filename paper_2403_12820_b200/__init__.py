@@ -16,7 +16,10 @@ from .scene import (BoundarySpec, ConfigError, GridPlane, IoError, MaterialParam
                     params_fingerprint, parse_scene)
 from .api import (BenchResult, ClothBatch, Context, CudaError, advance_with_impulse,  # noqa: E402
                   apply_dirichlet, benchmark_net, benchmark_sim, forward_impulse, nn_step,
-                  plug_impulse, rollout, simulate, step_semi_implicit, total_impulse)
+                  pinned_empty, plug_impulse, rollout, simulate, step_semi_implicit,
+                  total_impulse)
+from .trajio import (EvalReport, evaluate, export_obj, load_trajectory,  # noqa: E402
+                     save_trajectory, write_eval_csv)
 
 __all__ = [
     "BenchResult", "BoundarySpec", "ClothBatch", "ConfigError", "Context", "CudaError",
@@ -25,5 +28,7 @@ __all__ = [
     "apply_dirichlet", "benchmark_net", "build_grid", "channel_order_hash", "forward_impulse",
     "load_scene", "nn_step", "params_fingerprint", "parse_scene", "plug_impulse", "rollout",
     "benchmark_sim", "simulate", "step_semi_implicit", "total_impulse",
+    "EvalReport", "evaluate", "export_obj", "load_trajectory", "pinned_empty", "save_trajectory",
+    "write_eval_csv",
 ]
 __version__ = "0.1.0"

@@ -99,6 +99,8 @@ SIGNATURES = {
     "sc_pbs_step": (C.c_int, [_P, _P, _P, C.c_double, _P, _P, _P]),
     "sc_simulate_frames": (C.c_int, [_P, _P, _P, _I, _I, _P, _P]),
     "sc_benchmark_sim": (C.c_int, [_P, _I, _I, C.POINTER(C.c_double)]),
+    "sc_evaluate_frames": (C.c_int, [C.c_int, _P, _P, _I, C.c_int64, _P]),
+    "sc_eval_last_error": (C.c_char_p, []),
     "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),
     "sc_ctx_halo_elems": (C.c_int64, [_P]),

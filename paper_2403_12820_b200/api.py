@@ -156,11 +156,23 @@ class Context:
                                              MODES[mode], _ptr(xo), _ptr(vo), _ptr(m)))
         return (xo, vo, m) if constrained else (xo, vo)
 
-    def rollout_frames(self, x0, v0, steps: int, stride: int = 1, mode: str = "parity"):
+    def rollout_frames(self, x0, v0, steps: int, stride: int = 1, mode: str = "parity",
+                       out=None):
+        """Frames 0, stride, 2*stride, ... as [frames][batch][node][3] arrays. ``out`` = (fx, fv)
+        writes into caller arrays; page-locked ones (pinned_empty) take the D2H copies directly,
+        pageable ones go through the context's two pinned staging slots (overlapped)."""
         x0, v0 = self._arr(x0), self._arr(v0)
         nf = steps // stride + 1
-        fx = np.empty((nf,) + (self.batch, self.local_rows * self.nx, 3), self.dtype)
-        fv = np.empty_like(fx)
+        shape = (nf,) + (self.batch, self.local_rows * self.nx, 3)
+        if out is None:
+            fx = np.empty(shape, self.dtype)
+            fv = np.empty_like(fx)
+        else:
+            fx, fv = out
+            for a in (fx, fv):
+                if a.shape != shape or a.dtype != self.dtype or not a.flags.c_contiguous:
+                    raise ConfigError("frames: out arrays must be C-contiguous %s %s"
+                                      % (self.dtype.__name__, shape))
         _raise(self.lib, self.lib.sc_rollout_frames(self.h, _ptr(x0), _ptr(v0), int(steps),
                                                     int(stride), MODES[mode], _ptr(fx), _ptr(fv)))
         return fx, fv
@@ -264,6 +276,30 @@ class Context:
 
 
 # ---------------------------------------------------------------- reference-style API ----
+
+class _PinnedBlock:
+    def __init__(self, nbytes: int):
+        self.lib = _abi.load()
+        p = C.c_void_p()
+        _raise(self.lib, self.lib.sc_host_alloc(max(1, nbytes), C.byref(p)))
+        self.ptr = p.value
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            self.lib.sc_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """Uninitialised page-locked (cudaHostAlloc) numpy array; the block is freed with the array.
+    Frame and state transfers into such arrays are direct DMA, no staging copy."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    blk = _PinnedBlock(n)
+    buf = (C.c_char * max(1, n)).from_address(blk.ptr)
+    buf._owner = blk  # keep the allocation alive as long as any view of it
+    return np.frombuffer(buf, dt, count=int(np.prod(shape))).reshape(shape)
+
 
 def _state2(a, n: int, name: str) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float64)
@@ -514,3 +550,19 @@ class ClothBatch(Context):
     def __init__(self, scenes: Sequence[Scene], params: NetworkParams, precision: str = "f32",
                  device: int = 0, strip: Optional[tuple] = None):
         super().__init__(scenes, params, precision, device, strip)
+
+    def rollout_trajectories(self, steps: int, stride: int = 1, mode: str = "fast",
+                             pinned: bool = True) -> List[Trajectory]:
+        """Batched closed-loop rollout from every scene's pinned initial state (the batched form of
+        rollout, eval.cpp:86-103), one Trajectory per cloth holding frames 0, stride, 2*stride,
+        ... . Frame output streams off the device behind the stepping (§8(f3)); f32 frames are
+        widened to the Trajectory's double fields like read_trajectory does for CLT1 v2 files."""
+        x0 = np.stack([apply_dirichlet(s.initial_x, s.initial_v, s, 0.0)[0] for s in self.scenes])
+        v0 = np.stack([apply_dirichlet(s.initial_x, s.initial_v, s, 0.0)[1] for s in self.scenes])
+        nf = steps // stride + 1
+        shape = (nf, self.batch, self.local_rows * self.nx, 3)
+        out = (pinned_empty(shape, self.dtype), pinned_empty(shape, self.dtype)) if pinned else None
+        fx, fv = self.rollout_frames(x0, v0, steps, stride, mode, out=out)
+        return [Trajectory(self.nx, self.ny, s.dt * stride, s.spacing,
+                           fx[:, b].astype(np.float64), fv[:, b].astype(np.float64))
+                for b, s in enumerate(self.scenes)]

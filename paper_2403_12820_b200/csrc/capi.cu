@@ -135,6 +135,10 @@ struct sc_ctx {
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
   bool health_on = false;  // non-finite tracking in device-resident stepping
+  // frame streaming (sc_rollout_frames / sc_simulate_frames): two pinned host slots + events
+  void* pin_stage = nullptr;
+  size_t pin_stage_bytes = 0;
+  cudaEvent_t frame_ev[2] = {nullptr, nullptr};
 
   size_t elem() const { return prec == SC_F32 ? 4 : 8; }
   int64_t nodes_global() const { return static_cast<int64_t>(nx) * ny; }
@@ -529,6 +533,79 @@ void download_state(sc_ctx* c, int which, void* x, void* v, bool sync = true) {
   if (sync) ck(cudaStreamSynchronize(c->stream), "D2H sync");
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Frame output of a rollout (§8(f3)): frame f's AoS x/v are converted into device slot f&1 and
+// copied D2H behind the stepping kernels of frame f+1 on the same stream. Pinned destination
+// arrays are written directly; pageable ones go through two pinned slots, the host copying
+// frame f-1 out while the GPU advances frame f, so the device never waits on the host copy.
+template <typename StepFn>
+void frames_impl(sc_ctx* c, const void* x0, const void* v0, int steps, int stride, void* fx,
+                 void* fv, StepFn&& step) {
+  const size_t bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
+  upload_state(c, x0, v0);
+  std::memcpy(fx, x0, bytes);
+  std::memcpy(fv, v0, bytes);
+  const bool direct = is_pinned(fx) && is_pinned(fv);
+  c->aos.ensure(4 * bytes);
+  if (!direct && c->pin_stage_bytes < 4 * bytes) {
+    if (c->pin_stage) cudaFreeHost(c->pin_stage);
+    c->pin_stage = nullptr;
+    c->pin_stage_bytes = 0;
+    ck(cudaHostAlloc(&c->pin_stage, 4 * bytes, cudaHostAllocPortable), "cudaHostAlloc frames");
+    c->pin_stage_bytes = 4 * bytes;
+  }
+  for (cudaEvent_t& e : c->frame_ev)
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  auto* ux = static_cast<unsigned char*>(fx);
+  auto* uv = static_cast<unsigned char*>(fv);
+  auto* stage = static_cast<unsigned char*>(c->pin_stage);
+  auto drain = [&](int f) {  // host side of frame f (staged path)
+    const int slot = f & 1;
+    ck(cudaEventSynchronize(c->frame_ev[slot]), "frame event");
+    std::memcpy(ux + bytes * f, stage + 2 * bytes * slot, bytes);
+    std::memcpy(uv + bytes * f, stage + 2 * bytes * slot + bytes, bytes);
+  };
+  int f = 1;
+  for (int k = 0; k < steps; k += stride) {
+    const int n = std::min(stride, steps - k);
+    step(n, k);
+    if (n != stride) break;
+    const int slot = f & 1;
+    unsigned char* dx = c->aos.p + 2 * bytes * slot;
+    unsigned char* dv = dx + bytes;
+    cudaError_t e;
+    if (c->prec == SC_F32)
+      e = launch_planar_to_aos<float>(static_cast<const float*>(c->state[c->cur]),
+                                      reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
+                                      c->batch, c->nx, c->rows_local, c->plane_stride, c->pitch,
+                                      c->stream);
+    else
+      e = launch_planar_to_aos<double>(static_cast<const double*>(c->state[c->cur]),
+                                       reinterpret_cast<double*>(dx),
+                                       reinterpret_cast<double*>(dv), c->batch, c->nx,
+                                       c->rows_local, c->plane_stride, c->pitch, c->stream);
+    ck(e, "planar_to_aos");
+    c->launches.fetch_add(1);
+    unsigned char* hx = direct ? ux + bytes * f : stage + 2 * bytes * slot;
+    unsigned char* hv = direct ? uv + bytes * f : stage + 2 * bytes * slot + bytes;
+    ck(cudaMemcpyAsync(hx, dx, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H frame x");
+    ck(cudaMemcpyAsync(hv, dv, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H frame v");
+    ck(cudaEventRecord(c->frame_ev[slot], c->stream), "frame event");
+    if (!direct && f > 1) drain(f - 1);
+    ++f;
+  }
+  if (!direct && f > 1) drain(f - 1);
+  ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
 void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last,
                   int kind = KIND_STEP) {
   if (steps < 0) throw_config("steps: must be >= 0");
@@ -612,6 +689,9 @@ void sc_ctx_destroy(sc_ctx* c) {
   free_scene(c);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (cudaEvent_t e : c->frame_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->pin_stage) cudaFreeHost(c->pin_stage);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -796,21 +876,8 @@ sc_status sc_rollout_frames(sc_ctx* c, const void* x0, const void* v0, int32_t s
     if (!x0 || !v0 || !fx || !fv) throw_config("frames: null array");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_health(c);
-    upload_state(c, x0, v0);
-    const size_t frame_bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
-    std::memcpy(fx, x0, frame_bytes);
-    std::memcpy(fv, v0, frame_bytes);
-    int f = 1;
-    for (int k = 0; k < steps; k += stride) {
-      const int n = std::min(stride, steps - k);
-      advance_impl(c, n, k, mode, nullptr);
-      if (n == stride) {
-        download_state(c, c->cur, static_cast<unsigned char*>(fx) + frame_bytes * f,
-                       static_cast<unsigned char*>(fv) + frame_bytes * f);
-        ++f;
-      }
-    }
-    ck(cudaStreamSynchronize(c->stream), "sync");
+    frames_impl(c, x0, v0, steps, stride, fx, fv,
+                [&](int n, int k) { advance_impl(c, n, k, mode, nullptr); });
   });
 }
 
@@ -955,21 +1022,14 @@ sc_status sc_simulate_frames(sc_ctx* c, const void* x0, const void* v0, int32_t 
     const bool health_before = c->health_on;
     c->health_on = true;  // simulate_scene checks every step (sim.cpp:153)
     reset_health(c);
-    upload_state(c, x0, v0);
-    const size_t frame_bytes = static_cast<size_t>(c->batch) * c->nodes_local() * 3 * c->elem();
-    std::memcpy(fx, x0, frame_bytes);
-    std::memcpy(fv, v0, frame_bytes);
-    int f = 1;
-    for (int k = 0; k < steps; k += stride) {
-      const int n = std::min(stride, steps - k);
-      advance_impl(c, n, k, SC_MODE_PARITY, nullptr, KIND_PBS);
-      if (n == stride) {
-        download_state(c, c->cur, static_cast<unsigned char*>(fx) + frame_bytes * f,
-                       static_cast<unsigned char*>(fv) + frame_bytes * f);
-        ++f;
-      }
+    try {
+      frames_impl(c, x0, v0, steps, stride, fx, fv, [&](int n, int k) {
+        advance_impl(c, n, k, SC_MODE_PARITY, nullptr, KIND_PBS);
+      });
+    } catch (...) {
+      c->health_on = health_before;
+      throw;
     }
-    ck(cudaStreamSynchronize(c->stream), "sync");
     c->health_on = health_before;
   });
 }

@@ -378,6 +378,25 @@ class Trajectory:
         if f < 0 or f >= self.frame_count:
             raise ConfigError("frame index out of range")
 
+    def validate(self) -> None:
+        """Trajectory::validate (scene.cpp:63-75), same checks and messages."""
+        if self.nx < 2 or self.ny < 2:
+            raise ConfigError("trajectory: grid dimensions must be >= 2")
+        if not (self.dt > 0.0):
+            raise ConfigError("trajectory: dt must be > 0")
+        if not (self.spacing > 0.0):
+            raise ConfigError("trajectory: spacing must be > 0")
+        if self.frame_count < 1:
+            raise ConfigError("trajectory: needs at least one frame")
+        n = self.nx * self.ny
+        fx, fv = np.asarray(self.frames_x), np.asarray(self.frames_v)
+        if fx.ndim != 3 or fx.shape[1:] != (n, 3) or fv.shape != fx.shape:
+            raise ConfigError("trajectory: frame 0 has the wrong node count")
+        bad = ~(np.isfinite(fx).all(axis=(1, 2)) & np.isfinite(fv).all(axis=(1, 2)))
+        if bad.any():
+            raise ConfigError("trajectory: frame %d has non-finite components"
+                              % int(np.argmax(bad)))
+
     def positions(self, frame: int) -> np.ndarray:
         self._check(frame)
         return np.array(self.frames_x[frame], dtype=np.float64)
