@@ -202,6 +202,66 @@ sc_status sc_evaluate_frames(int device, const double* test_x, const double* ref
                              int32_t frames, int64_t nodes, double* frame_sums);
 const char* sc_eval_last_error(void);
 
+/* ---- training forward + backward (§8(f1), train.hpp / train.cpp, net.cpp:144-201) --------- */
+/* A trainer holds one scene (batch 1, f64) and its ground-truth trajectory resident on the GPU
+ * ([frames][node][3] f64 host arrays, copied once). Results are bit-identical to the reference's
+ * sample_batch / compute_loss / backward_gradients / train_loop (see csrc/train.cu). */
+typedef struct sc_trainer sc_trainer;
+
+/* TrainConfig (train.hpp:16-53); schedule_kind 0 = Step, 1 = Cosine; freeze_mask bit g freezes
+ * ParamGroup g (kernel=0, linear, bias, nonlinear, deriv, self_velocity, alpha=6). */
+typedef struct sc_train_config {
+  double alpha;
+  int32_t batch_size, epochs;
+  int32_t schedule_kind;
+  double lr0, gamma;
+  int32_t interval;
+  double floor;
+  int32_t period;
+  uint64_t seed;
+  int32_t de_population, de_generations;
+  double de_bound, de_cross_prob, de_diff_weight;
+  int32_t de_probe_batch;
+  int32_t checkpoint_interval;
+  uint32_t freeze_mask;
+} sc_train_config;
+
+/* AdamState (train.hpp:118-123) over the flat 53 scalars. */
+typedef struct sc_adam_state {
+  double m[53];
+  double v[53];
+  int64_t step;
+} sc_adam_state;
+
+sc_status sc_trainer_create(int device, const sc_scene_desc* scene, int32_t frames,
+                            const double* frames_x, const double* frames_v, sc_trainer** out);
+void sc_trainer_destroy(sc_trainer* trainer);
+/* sample_batch (train.cpp:91-127) with a fresh Rng(rng_seed): batch indices (nullable) and the
+ * force-integration targets f_k*dt [batch][node][3] (nullable); the batch becomes current. */
+sc_status sc_trainer_sample_batch(sc_trainer* trainer, int32_t batch_size, uint64_t rng_seed,
+                                  int32_t* indices_out, double* force_dt_out);
+/* The index draw of sample_batch alone (host only, no device): batch_size distinct transitions
+ * of a frames-long trajectory from Rng(rng_seed). */
+sc_status sc_sample_indices(int32_t frames, int32_t batch_size, uint64_t rng_seed,
+                            int32_t* indices_out);
+/* Explicit transition indices as the current batch (targets computed on the device). */
+sc_status sc_trainer_set_batch(sc_trainer* trainer, const int32_t* indices, int32_t count);
+/* compute_loss (train.cpp:129-209) on the current batch: loss_out = {total, physics, data};
+ * grads_out (53, for_each_gradient order, nullable) = the ParamGradients. */
+sc_status sc_trainer_compute_loss(sc_trainer* trainer, const sc_params* params, double alpha,
+                                  double* loss_out, double* grads_out);
+/* train_loop (train.cpp:343-375): DE pre-search + Adam epochs, or fine-tune from resume_params
+ * (+ trainable flags, + the Adam state in opt_inout). history_out: epochs x {step, lr, physics,
+ * data, total} (nullable); opt_inout (nullable) receives the final Adam state. */
+sc_status sc_trainer_run(sc_trainer* trainer, const sc_train_config* cfg,
+                         const sc_params* resume_params, const uint8_t* resume_trainable,
+                         sc_adam_state* opt_inout, sc_params* params_out, uint8_t* trainable_out,
+                         double* history_out);
+/* backward_gradients (net.cpp:144-201) for one state and upstream cotangent [node][3]. */
+sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double* x,
+                                const double* v, const sc_params* params, const double* upstream,
+                                double* grads_out);
+
 /* benchmark_sim (eval.hpp:46 / eval.cpp:151-153): device-timed PBS steps from the ctx state. */
 sc_status sc_benchmark_sim(sc_ctx* ctx, int32_t steps, int32_t warmup, double* seconds);
 

@@ -149,6 +149,12 @@ class Reference:
         L.ref_benchmark_net_cloth_parallel.argtypes = [_I, _I, _I, _CD, _PR, _P, _P, _I, _I,
                                                        C.POINTER(C.c_double),
                                                        C.POINTER(C.c_double)]
+        _TC = C.POINTER(_abi.sc_train_config)
+        L.ref_sample_batch.argtypes = [_I, _I, _CD, _I, _P, _P, _I, C.c_uint64, _P, _P]
+        L.ref_compute_loss.argtypes = [_I, _I, _CD, _I, _P, _P, _I, C.c_uint64, _PR, C.c_double,
+                                       _I, _P, _P]
+        L.ref_backward_gradients.argtypes = [_I, _I, _P, _P, _PR, _P, _P]
+        L.ref_train.argtypes = [_I, _I, _CD, _I, _P, _P, _TC, _PR, _P, _P]
 
     def _ck(self, rc):
         if rc != 0:
@@ -263,3 +269,40 @@ class Reference:
             nx, ny, batch, C.cast(arr, _CD), C.byref(params), _p(x0), _p(v0), steps, warmup,
             C.byref(mx), C.byref(wall)))
         return mx.value, wall.value
+
+    # ---- training (train.cpp / net.cpp:144-201) -------------------------------------------
+    def sample_batch(self, nx, ny, cloth, fx, fv, batch_size, seed):
+        fx = np.ascontiguousarray(fx, np.float64)
+        fv = np.ascontiguousarray(fv, np.float64)
+        idx = np.empty(batch_size, np.int32)
+        tgt = np.empty((batch_size, nx * ny, 3))
+        self._ck(self.lib.ref_sample_batch(nx, ny, C.byref(cloth), fx.shape[0], _p(fx), _p(fv),
+                                           batch_size, seed, _p(idx), _p(tgt)))
+        return idx, tgt
+
+    def compute_loss(self, nx, ny, cloth, fx, fv, batch_size, seed, params, alpha, grads=True):
+        fx = np.ascontiguousarray(fx, np.float64)
+        fv = np.ascontiguousarray(fv, np.float64)
+        loss = np.empty(3)
+        g = np.empty(53)
+        self._ck(self.lib.ref_compute_loss(nx, ny, C.byref(cloth), fx.shape[0], _p(fx), _p(fv),
+                                           batch_size, seed, C.byref(params), alpha, int(grads),
+                                           _p(loss), _p(g)))
+        return loss, (g if grads else None)
+
+    def backward_gradients(self, nx, ny, x, v, params, upstream):
+        g = np.empty(53)
+        self._ck(self.lib.ref_backward_gradients(
+            nx, ny, _p(np.ascontiguousarray(x, np.float64)), _p(np.ascontiguousarray(v, np.float64)),
+            C.byref(params), _p(np.ascontiguousarray(upstream, np.float64)), _p(g)))
+        return g
+
+    def train(self, nx, ny, cloth, fx, fv, cfg):
+        fx = np.ascontiguousarray(fx, np.float64)
+        fv = np.ascontiguousarray(fv, np.float64)
+        out = _abi.sc_params()
+        tr = np.zeros(7, np.uint8)
+        hist = np.zeros((cfg.epochs, 5))
+        self._ck(self.lib.ref_train(nx, ny, C.byref(cloth), fx.shape[0], _p(fx), _p(fv),
+                                    C.byref(cfg), C.byref(out), _p(tr), _p(hist)))
+        return out, tr, hist

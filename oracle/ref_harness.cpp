@@ -28,6 +28,7 @@
 #include "cloth/net.hpp"
 #include "cloth/sim.hpp"
 #include "cloth/threads.hpp"
+#include "cloth/train.hpp"
 
 #include "../include/stencilcloth_b200.h"
 
@@ -418,6 +419,137 @@ int ref_benchmark_net_cloth_parallel(int nx, int ny, int ncloth, const sc_cloth_
     *wall_seconds = std::chrono::duration<double>(t1 - t0).count();
   });
 }
+
+// ---- training (train.cpp, net.cpp:144-201): the reference's own sample_batch / compute_loss /
+// backward_gradients / train_loop over a trajectory given as [frames][n][3] arrays.
+namespace {
+Trajectory make_traj(int nx, int ny, const sc_cloth_desc* cd, int frames, const double* fx,
+                     const double* fv) {
+  Trajectory t;
+  t.nx = nx;
+  t.ny = ny;
+  t.dt = cd->dt;
+  t.spacing = cd->spacing > 0.0 ? cd->spacing : 1.0 / (nx - 1);
+  const size_t n = static_cast<size_t>(nx) * ny;
+  t.frames.resize(static_cast<size_t>(frames));
+  for (int f = 0; f < frames; ++f) {
+    copy_in(t.frames[static_cast<size_t>(f)].x, fx + 3 * n * f, n);
+    copy_in(t.frames[static_cast<size_t>(f)].v, fv + 3 * n * f, n);
+  }
+  return t;
+}
+void flat_grads(const ParamGradients& g, double* out) {
+  ParamGradients c = g;
+  int k = 0;
+  for_each_gradient(c, [&](ParamGroup, int, double& v) { out[k++] = v; });
+}
+}  // namespace
+
+extern "C" {
+
+int ref_sample_batch(int nx, int ny, const sc_cloth_desc* cd, int frames, const double* fx,
+                     const double* fv, int batch_size, uint64_t seed, int32_t* idx_out,
+                     double* force_dt_out) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, fx, fv);
+    const Trajectory traj = make_traj(nx, ny, cd, frames, fx, fv);
+    Rng rng(seed);
+    const TrainBatch b = sample_batch(traj, scene, batch_size, rng);
+    const size_t n = static_cast<size_t>(nx) * ny;
+    for (size_t k = 0; k < b.indices.size(); ++k) {
+      if (idx_out) idx_out[k] = b.indices[k];
+      if (force_dt_out) copy_out(force_dt_out + 3 * n * k, b.force_dt[k]);
+    }
+  });
+}
+
+int ref_compute_loss(int nx, int ny, const sc_cloth_desc* cd, int frames, const double* fx,
+                     const double* fv, int batch_size, uint64_t seed, const sc_params* p,
+                     double alpha, int want_grads, double* loss_out, double* grads_out) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, fx, fv);
+    const Trajectory traj = make_traj(nx, ny, cd, frames, fx, fv);
+    Rng rng(seed);
+    TrainBatch b = sample_batch(traj, scene, batch_size, rng);
+    b.traj = &traj;
+    b.scene = &scene;
+    ParamGradients g;
+    const LossValue l = compute_loss(to_params(p), b, alpha, want_grads ? &g : nullptr);
+    loss_out[0] = l.total;
+    loss_out[1] = l.physics;
+    loss_out[2] = l.data;
+    if (want_grads) flat_grads(g, grads_out);
+  });
+}
+
+int ref_backward_gradients(int nx, int ny, const double* x, const double* v, const sc_params* p,
+                           const double* upstream, double* grads_out) {
+  return guarded([&] {
+    const GridInit g = build_grid(nx, ny, 1.0, Vec3{}, GridPlane::XY);
+    ClothState s;
+    const size_t n = static_cast<size_t>(nx) * ny;
+    copy_in(s.x, x, n);
+    copy_in(s.v, v, n);
+    Vec3Field u;
+    copy_in(u, upstream, n);
+    flat_grads(backward_gradients(s, g.topology, to_params(p), u), grads_out);
+  });
+}
+
+int ref_train(int nx, int ny, const sc_cloth_desc* cd, int frames, const double* fx,
+              const double* fv, const sc_train_config* c, sc_params* params_out,
+              uint8_t* trainable_out, double* history_out) {
+  return guarded([&] {
+    const Scene scene = to_scene(nx, ny, cd, fx, fv);
+    const Trajectory traj = make_traj(nx, ny, cd, frames, fx, fv);
+    TrainConfig cfg;
+    cfg.alpha = c->alpha;
+    cfg.batch_size = c->batch_size;
+    cfg.epochs = c->epochs;
+    cfg.schedule.kind = c->schedule_kind ? ScheduleKind::Cosine : ScheduleKind::Step;
+    cfg.schedule.lr0 = c->lr0;
+    cfg.schedule.gamma = c->gamma;
+    cfg.schedule.interval = c->interval;
+    cfg.schedule.floor = c->floor;
+    cfg.schedule.period = c->period;
+    cfg.seed = c->seed;
+    cfg.de.population = c->de_population;
+    cfg.de.generations = c->de_generations;
+    cfg.de.bound = c->de_bound;
+    cfg.de.cross_prob = c->de_cross_prob;
+    cfg.de.diff_weight = c->de_diff_weight;
+    cfg.de.probe_batch = c->de_probe_batch;
+    cfg.checkpoint_interval = c->checkpoint_interval;
+    for (int g = 0; g < kParamGroups; ++g)
+      if (c->freeze_mask & (1u << g)) cfg.freeze.push_back(static_cast<ParamGroup>(g));
+    const TrainResult r = train_loop(cfg, scene, traj);
+    NetworkParams q = r.params;
+    int k = 0;
+    double flat[NetworkParams::kScalarCount];
+    for_each_scalar(q, [&](ParamGroup, int, double& v) { flat[k++] = v; });
+    for (int i = 0; i < kChannels; ++i) {
+      params_out->kernel_gain[i] = flat[i];
+      params_out->linear_w[i] = flat[12 + i];
+      params_out->nonlinear_w[i] = flat[27 + i];
+      params_out->deriv_w[i] = flat[39 + i];
+    }
+    for (int d = 0; d < 3; ++d) params_out->linear_b[d] = flat[24 + d];
+    params_out->self_velocity_w = flat[51];
+    params_out->isru_alpha = flat[52];
+    for (int g = 0; g < kParamGroups; ++g)
+      if (trainable_out) trainable_out[g] = q.is_trainable(static_cast<ParamGroup>(g)) ? 1 : 0;
+    if (history_out)
+      for (size_t e = 0; e < r.history.size(); ++e) {
+        history_out[5 * e] = r.history[e].step;
+        history_out[5 * e + 1] = r.history[e].lr;
+        history_out[5 * e + 2] = r.history[e].physics;
+        history_out[5 * e + 3] = r.history[e].data;
+        history_out[5 * e + 4] = r.history[e].total;
+      }
+  });
+}
+
+}  // extern "C"
 
 // Scene JSON parsing through the reference parser (io.cpp:199-359), for checking the Python
 // mirror's parser. Returns counts; arrays are filled when non-null and large enough.

@@ -18,6 +18,10 @@ from .api import (BenchResult, ClothBatch, Context, CudaError, advance_with_impu
                   apply_dirichlet, benchmark_net, benchmark_sim, forward_impulse, nn_step,
                   pinned_empty, plug_impulse, rollout, simulate, step_semi_implicit,
                   total_impulse)
+from .training import (AdamState, DeConfig, LossRow, LossValue, ParamGradients,  # noqa: E402
+                    ScheduleConfig, ScheduleKind, TrainConfig, Trainer, TrainResult,
+                    backward_gradients, gradient_check, sample_indices, train,
+                       train_loop)
 from .trajio import (EvalReport, evaluate, export_obj, load_trajectory,  # noqa: E402
                      save_trajectory, write_eval_csv)
 
@@ -29,6 +33,8 @@ __all__ = [
     "load_scene", "nn_step", "params_fingerprint", "parse_scene", "plug_impulse", "rollout",
     "benchmark_sim", "simulate", "step_semi_implicit", "total_impulse",
     "EvalReport", "evaluate", "export_obj", "load_trajectory", "pinned_empty", "save_trajectory",
-    "write_eval_csv",
+    "write_eval_csv", "AdamState", "DeConfig", "LossRow", "LossValue", "ParamGradients",
+    "ScheduleConfig", "ScheduleKind", "TrainConfig", "Trainer", "TrainResult",
+    "backward_gradients", "gradient_check", "sample_indices", "train", "train_loop",
 ]
 __version__ = "0.1.0"

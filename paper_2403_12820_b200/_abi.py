@@ -30,6 +30,34 @@ class sc_params(C.Structure):
     ]
 
 
+class sc_train_config(C.Structure):
+    """TrainConfig (train.hpp:16-53) as the C-ABI carries it."""
+    _fields_ = [
+        ("alpha", C.c_double),
+        ("batch_size", C.c_int32),
+        ("epochs", C.c_int32),
+        ("schedule_kind", C.c_int32),
+        ("lr0", C.c_double),
+        ("gamma", C.c_double),
+        ("interval", C.c_int32),
+        ("floor", C.c_double),
+        ("period", C.c_int32),
+        ("seed", C.c_uint64),
+        ("de_population", C.c_int32),
+        ("de_generations", C.c_int32),
+        ("de_bound", C.c_double),
+        ("de_cross_prob", C.c_double),
+        ("de_diff_weight", C.c_double),
+        ("de_probe_batch", C.c_int32),
+        ("checkpoint_interval", C.c_int32),
+        ("freeze_mask", C.c_uint32),
+    ]
+
+
+class sc_adam_state(C.Structure):
+    _fields_ = [("m", C.c_double * 53), ("v", C.c_double * 53), ("step", C.c_int64)]
+
+
 class sc_sphere(C.Structure):
     _fields_ = [("center", C.c_double * 3), ("radius", C.c_double), ("friction", C.c_double)]
 
@@ -101,6 +129,15 @@ SIGNATURES = {
     "sc_benchmark_sim": (C.c_int, [_P, _I, _I, C.POINTER(C.c_double)]),
     "sc_evaluate_frames": (C.c_int, [C.c_int, _P, _P, _I, C.c_int64, _P]),
     "sc_eval_last_error": (C.c_char_p, []),
+    "sc_trainer_create": (C.c_int, [C.c_int, _P, _I, _P, _P, C.POINTER(_P)]),
+    "sc_trainer_destroy": (None, [_P]),
+    "sc_trainer_sample_batch": (C.c_int, [_P, _I, C.c_uint64, _P, _P]),
+    "sc_trainer_set_batch": (C.c_int, [_P, _P, _I]),
+    "sc_sample_indices": (C.c_int, [_I, _I, C.c_uint64, _P]),
+    "sc_trainer_compute_loss": (C.c_int, [_P, C.POINTER(sc_params), C.c_double, _P, _P]),
+    "sc_trainer_run": (C.c_int, [_P, C.POINTER(sc_train_config), C.POINTER(sc_params), _P,
+                                 C.POINTER(sc_adam_state), C.POINTER(sc_params), _P, _P]),
+    "sc_backward_gradients": (C.c_int, [C.c_int, _I, _I, _P, _P, C.POINTER(sc_params), _P, _P]),
     "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),
     "sc_ctx_halo_elems": (C.c_int64, [_P]),
@@ -119,6 +156,7 @@ SIGNATURES = {
     "sc_ctx_launch_count": (C.c_int64, [_P]),
     # host-side seeded generators (csrc/host_gen.cpp)
     "sc_rng_mix": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "sc_mt64_fill": (None, [C.c_uint64, C.c_int64, _P]),
     "sc_rng_uniform01": (None, [C.c_uint64, C.c_int64, _P]),
     "sc_rng_normal": (None, [C.c_uint64, C.c_int64, C.c_double, _P]),
     "sc_gen_sheet": (

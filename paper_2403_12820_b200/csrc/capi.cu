@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/stencilcloth_b200.h"
+#include "capi_internal.h"
 #include "sc_device.cuh"
 #include "sc_kernels.h"
 
@@ -1207,3 +1208,24 @@ sc_status sc_debug_unit_timing(void* dev_buf) {
 int64_t sc_debug_units(sc_ctx* c) { return c ? c->plan.units : 0; }
 
 }  // extern "C"
+
+namespace scb {
+
+bool ctx_scene_view(sc_ctx* c, SceneView* v) {
+  if (!c || !c->has_scene || c->rows_local != c->ny) return false;
+  v->cloths = c->cloths;
+  v->spheres = c->spheres;
+  v->planes = c->planes;
+  v->anchors = c->anchors;
+  v->pin_bits = c->pin_bits.p;
+  v->pin_rank = c->pin_rank.p;
+  v->nx = c->nx;
+  v->ny = c->ny;
+  v->batch = c->batch;
+  v->device = c->device;
+  return true;
+}
+
+void set_last_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace scb

@@ -45,6 +45,13 @@ extern "C" {
 
 uint64_t sc_rng_mix(uint64_t seed, uint64_t stream) { return mix(seed, stream); }
 
+// the first `count` raw outputs of std::mt19937_64(seed): the engine under cloth::Rng
+// (rng.hpp:13-47), whose fixed-algorithm draws the Python layer builds on
+void sc_mt64_fill(uint64_t seed, int64_t count, uint64_t* out) {
+  std::mt19937_64 g(seed);
+  for (int64_t i = 0; i < count; ++i) out[i] = g();
+}
+
 // count uniforms in [0,1) from one stream
 void sc_rng_uniform01(uint64_t seed, int64_t count, double* out) {
   Gen g(seed);

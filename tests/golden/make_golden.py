@@ -23,8 +23,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from golden_io import GOLDEN_DIR, cloth_desc, params_c, scene_arrays  # noqa: E402
 from oracle.pyoracle import Reference  # noqa: E402
+from paper_2403_12820_b200 import _abi  # noqa: E402
 
-R = Reference()
+# the reference is only needed to generate; tests import the helpers below without it
+R = Reference() if __name__ == "__main__" else None
 
 
 def sheet(rng, nx, ny, spacing, noise, origin=(0.0, 0.0, 0.0)):
@@ -184,7 +186,57 @@ def pbs_main():
     save("pbs_steps32", **sc, x0=x32, v0=v32, checkpoints=np.array([1, 20, 100]), **outs)
 
 
+def train_config(**kw):
+    c = _abi.sc_train_config()
+    base = dict(alpha=0.5, batch_size=8, epochs=12, schedule_kind=0, lr0=1e-2, gamma=0.5,
+                interval=5, floor=1e-5, period=1000, seed=3, de_population=6, de_generations=2,
+                de_bound=4.0, de_cross_prob=0.9, de_diff_weight=0.7, de_probe_batch=4,
+                checkpoint_interval=500, freeze_mask=0)
+    base.update(kw)
+    for k, v in base.items():
+        setattr(c, k, v)
+    return c
+
+
+def train_main():
+    """Training forward/backward fixtures from the reference's own
+    sample_batch / compute_loss / backward_gradients / train_loop (train.cpp, net.cpp)."""
+    rng = np.random.default_rng(20240321)
+    nx, ny = 12, 10
+    sp = 0.05
+    x0 = sheet(rng, nx, ny, sp, 1e-3, origin=(-0.275, -0.225, 0.28))
+    pins = [0, nx - 1]
+    sc = scene_arrays(nx, ny, 1e-3, mass=0.01, drag=0.03, pressure=0.4, gravity=(0.0, 0.0, -9.8),
+                      plugs=(0, 1, 1), pin_nodes=pins, pin_anchors=x0[pins],
+                      pin_velocity=(0.02, 0.0, 0.0), spheres=[(0.0, 0.0, 0.0, 0.25, 0.3)],
+                      stiffness=40.0, damping=0.2, spacing=sp)
+    keep = []
+    cd = cloth_desc(sc, keep)
+    fx, fv = R.simulate_f64(nx, ny, cd, x0, np.zeros_like(x0), 60)
+    idx, tgt = R.sample_batch(nx, ny, cd, fx, fv, 16, 77)
+    p = random_params(rng, sigma=0.05, gains=True, alpha=1.2)
+    loss, grads = R.compute_loss(nx, ny, cd, fx, fv, 16, 77, params_c(p), 0.3)
+    bx, by = 40, 30  # two backward chunks of 1024 nodes
+    bxs = sheet(rng, bx, by, 0.1, 0.03)
+    bvs = rng.uniform(-1.0, 1.0, bxs.shape)
+    bup = rng.normal(0.0, 1.0, bxs.shape)
+    bp = random_params(rng, sigma=0.4, gains=True, alpha=0.8)
+    bgrads = R.backward_gradients(bx, by, bxs, bvs, params_c(bp), bup)
+    cfg = train_config()
+    tp, ttr, thist = R.train(nx, ny, cd, fx, fv, cfg)
+    flat = (list(tp.kernel_gain) + list(tp.linear_w) + list(tp.linear_b) + list(tp.nonlinear_w)
+            + list(tp.deriv_w) + [tp.self_velocity_w, tp.isru_alpha])
+    save("train_f64", **sc, frames_x=fx, frames_v=fv, batch_seed=np.uint64(77), batch_idx=idx,
+         targets=tgt, params=p, loss_alpha=np.float64(0.3), loss=loss, grads=grads,
+         bwd_dims=np.array([bx, by]), bwd_x=bxs, bwd_v=bvs, bwd_up=bup, bwd_params=bp,
+         bwd_grads=bgrads, train_params=np.array(flat), train_trainable=ttr, train_history=thist)
+
+
 if __name__ == "__main__":
+    if "--train" in sys.argv:
+        train_main()
+        sys.exit(0)
     if "--pbs" not in sys.argv:
         main()
     pbs_main()
+    train_main()
