@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <random>
 #include <string>
 #include <vector>
@@ -71,6 +72,9 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
   void ensure(size_t count) {
     if (count <= n && p) return;
     if (p) cudaFree(p);
@@ -319,29 +323,98 @@ __global__ void __launch_bounds__(256) loss_fwd_kernel(const LossArgs a) {
   }
 }
 
-// The loss sums as the reference's single sequential chain (train.cpp:168-182); records the
-// first batch element after which either running sum is non-finite.
-__global__ void loss_chain_kernel(const double* __restrict__ pt, const double* __restrict__ dt,
-                                  int batch, int64_t n, double* out, int32_t* bad_b) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double ps = 0.0, ds = 0.0;
+// The loss sums as the reference's sequential chain (train.cpp:168-182): phys_sq and data_sq are
+// two independent chains over (batch element, node), so lane 0 of warp 0 runs the first and
+// lane 0 of warp 1 the second while the whole block stages the next tile in shared memory
+// (the chain is bound by the dependent-add latency, never by a load). Each records the first
+// batch element after which its running sum is non-finite; the reference stops at the smaller.
+constexpr int kChainTile = 1024;
+
+__global__ void __launch_bounds__(256) loss_chain_kernel(const double* __restrict__ pt,
+                                                         const double* __restrict__ dt,
+                                                         int batch, int64_t n, double* out,
+                                                         int32_t* bad_b) {
+  __shared__ double buf[2][2][kChainTile];
+  __shared__ int bad_s[2];
+  const int64_t total = static_cast<int64_t>(batch) * n;
+  const int64_t tiles = (total + kChainTile - 1) / kChainTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warps 2..7 stage tiles (all loads of a tile in flight at once); the two consumer warps
+  // never wait on a global load
+  constexpr int kLoaders = 192, kPer = (kChainTile + kLoaders - 1) / kLoaders;
+  auto load = [&](int64_t t) {
+    if (threadIdx.x < 64) return;
+    const int64_t g0 = t * kChainTile;
+    const int l = threadIdx.x - 64;
+    double a[kPer], c[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int j = l + u * kLoaders;
+      const int64_t g = g0 + j;
+      const bool ok = j < kChainTile && g < total;
+      a[u] = ok ? __ldg(pt + g) : 0.0;
+      c[u] = ok ? __ldg(dt + g) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int j = l + u * kLoaders;
+      if (j < kChainTile) {
+        buf[t & 1][0][j] = a[u];
+        buf[t & 1][1][j] = c[u];
+      }
+    }
+  };
+  load(0);
+  __syncthreads();
+  const bool consumer = warp < 2 && lane == 0;
+  double acc = 0.0;
   int bad = kNone;
-  for (int b = 0; b < batch; ++b) {
-    const double* p = pt + static_cast<int64_t>(b) * n;
-    const double* q = dt + static_cast<int64_t>(b) * n;
-#pragma unroll 8
-    for (int64_t i = 0; i < n; ++i) {
-      ps = R::add(ps, __ldg(p + i));
-      ds = R::add(ds, __ldg(q + i));
+  int b = 0;
+  int64_t boundary = n;  // global index one past batch element b
+  for (int64_t t = 0; t < tiles; ++t) {
+    if (t + 1 < tiles) load(t + 1);
+    if (consumer && bad == kNone) {
+      const double* src = buf[t & 1][warp];
+      const int64_t g0 = t * kChainTile;
+      const int len = static_cast<int>(total - g0 < kChainTile ? total - g0 : kChainTile);
+      int j = 0;
+      while (j < len && bad == kNone) {
+        const int seg = static_cast<int>(boundary - g0 < len ? boundary - g0 : len);
+        // software-pipelined: the next eight values are loaded while the current eight are
+        // added, so the chain runs at the dependent-add latency
+        if (j + 8 <= seg) {
+          double cur[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cur[u] = src[j + u];
+          for (; j + 16 <= seg; j += 8) {
+            double nxt[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nxt[u] = src[j + 8 + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = R::add(acc, cur[u]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = R::add(acc, cur[u]);
+          j += 8;
+        }
+        for (; j < seg; ++j) acc = R::add(acc, src[j]);
+        if (g0 + j == boundary) {
+          if (!isfinite(acc)) bad = b;
+          ++b;
+          boundary += n;
+        }
+      }
     }
-    if (!isfinite(ps) || !isfinite(ds)) {
-      bad = b;
-      break;
-    }
+    __syncthreads();
   }
-  out[0] = ps;
-  out[1] = ds;
-  *bad_b = bad;
+  if (consumer) {
+    out[warp] = acc;
+    bad_s[warp] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *bad_b = bad_s[0] < bad_s[1] ? bad_s[0] : bad_s[1];
 }
 
 // backward_gradients per-node terms (net.cpp:159-196) into [b][chunk][term][kChunk].
@@ -443,29 +516,71 @@ __global__ void __launch_bounds__(256) bwd_terms_kernel(const BwdArgs a) {
 
 // One sequential chain per scalar over a chunk's nodes (alpha: over (node, channel)); output
 // in for_each_gradient order (kernel, linear, bias, nonlinear, deriv, self_velocity, alpha).
-__global__ void __launch_bounds__(64) bwd_reduce_kernel(const double* __restrict__ terms,
-                                                        int64_t n, int chunks,
-                                                        double* __restrict__ partial) {
+// The block stages 32-node tiles of all 64 term rows in shared memory (double buffered) so the
+// 53 chains run at dependent-add latency.
+constexpr int kRedTile = 32;
+
+__global__ void __launch_bounds__(256) bwd_reduce_kernel(const double* __restrict__ terms,
+                                                         int64_t n, int chunks,
+                                                         double* __restrict__ partial) {
+  __shared__ double tile[2][kTerms][kRedTile];
   const int bc = blockIdx.x;  // (batch element in group) * chunks + chunk
   const int chunk = bc % chunks;
   const int64_t rem = n - static_cast<int64_t>(chunk) * kChunk;
   const int len = rem < kChunk ? static_cast<int>(rem) : kChunk;
+  const int ntiles = (len + kRedTile - 1) / kRedTile;
   const double* T = terms + static_cast<int64_t>(bc) * kTerms * kChunk;
+  // warps 2.. stage tiles; the 53 chain threads (warps 0-1) never wait on a global load
+  constexpr int kLoaders = 192, kPer = (kTerms * kRedTile + kLoaders - 1) / kLoaders;
+  auto load = [&](int t) {
+    if (threadIdx.x < 64) return;
+    const int l = threadIdx.x - 64;
+    double a[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = l + u * kLoaders;
+      const int row = e / kRedTile, j = e - row * kRedTile;
+      a[u] = e < kTerms * kRedTile
+                 ? __ldg(T + static_cast<int64_t>(row) * kChunk + t * kRedTile + j)
+                 : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = l + u * kLoaders;
+      if (e < kTerms * kRedTile) tile[t & 1][e / kRedTile][e % kRedTile] = a[u];
+    }
+  };
+  load(0);
+  __syncthreads();
   const int r = threadIdx.x;
   double acc = 0.0;
-  if (r < kTermAlpha) {
-    const double* row = T + static_cast<int64_t>(r) * kChunk;
+  for (int t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) load(t + 1);
+    const int cnt = len - t * kRedTile < kRedTile ? len - t * kRedTile : kRedTile;
+    if (r < kTermAlpha) {
+      const double* row = tile[t & 1][r];
 #pragma unroll 8
-    for (int i = 0; i < len; ++i) acc = R::add(acc, __ldg(row + i));
-    partial[static_cast<int64_t>(bc) * kScalars + r] = acc;
-  } else if (r == kTermAlpha) {
-    const double* row = T + static_cast<int64_t>(kTermAlpha) * kChunk;
-    for (int i = 0; i < len; ++i) {
+      for (int i = 0; i < cnt; ++i) acc = R::add(acc, row[i]);
+    } else if (r == kTermAlpha) {
+      int i = 0;
+      for (; i + 2 <= cnt; i += 2) {  // both nodes' 24 terms loaded ahead of the chain
+        double v[2 * kChannels];
 #pragma unroll
-      for (int c = 0; c < kChannels; ++c) acc = R::add(acc, __ldg(row + c * kChunk + i));
+        for (int c = 0; c < kChannels; ++c) {
+          v[c] = tile[t & 1][kTermAlpha + c][i];
+          v[kChannels + c] = tile[t & 1][kTermAlpha + c][i + 1];
+        }
+#pragma unroll
+        for (int q = 0; q < 2 * kChannels; ++q) acc = R::add(acc, v[q]);
+      }
+      for (; i < cnt; ++i) {
+#pragma unroll
+        for (int c = 0; c < kChannels; ++c) acc = R::add(acc, tile[t & 1][kTermAlpha + c][i]);
+      }
     }
-    partial[static_cast<int64_t>(bc) * kScalars + kScalars - 1] = acc;
+    __syncthreads();
   }
+  if (r <= kTermAlpha) partial[static_cast<int64_t>(bc) * kScalars + r] = acc;
 }
 
 // total.add_scaled(partial, 1.0) over chunks (net.cpp:198-199), then grads.add_scaled(g, 1.0)
@@ -475,11 +590,24 @@ __global__ void bwd_final_kernel(const double* __restrict__ partial, int nb, int
   const int s = threadIdx.x;
   if (s >= kScalars) return;
   double g = grads[s];
-  for (int b = 0; b < nb; ++b) {
-    double tot = 0.0;
-    for (int c = 0; c < chunks; ++c)
-      tot = R::add(tot, R::mul(partial[(static_cast<int64_t>(b) * chunks + c) * kScalars + s], 1.0));
-    g = R::add(g, R::mul(tot, 1.0));
+  double tot = 0.0;
+  const int64_t total = static_cast<int64_t>(nb) * chunks;
+  int c = 0;
+  for (int64_t k0 = 0; k0 < total; k0 += 8) {  // eight partials loaded ahead of the chain
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = k0 + u < total ? __ldg(partial + (k0 + u) * kScalars + s) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (k0 + u >= total) break;
+      tot = R::add(tot, R::mul(v[u], 1.0));
+      if (++c == chunks) {
+        g = R::add(g, R::mul(tot, 1.0));
+        tot = 0.0;
+        c = 0;
+      }
+    }
   }
   grads[s] = g;
 }
@@ -589,15 +717,35 @@ struct sc_trainer {
   int plug_p = 0, plug_g = 0, plug_d = 0;
   int n_pins = 0;
   double dt = 0.0, mass = 1.0;
-  cudaStream_t s0 = nullptr, s1 = nullptr;
-  cudaEvent_t ev_fwd = nullptr, ev_chain = nullptr;
+  cudaStream_t s0 = nullptr;
   DBuf<double> fx, fv;
   Batch batch;  // the batch set through the C-ABI
   // compute_loss scratch
-  DBuf<double> rp, rd, pt, dtm, terms, partial, grads, chain_out;
+  DBuf<double> rp, rd, terms, partial, grads;
   DBuf<unsigned long long> count;
-  DBuf<int32_t> bad_fwd, bad_b, bad_spring;
+  DBuf<int32_t> bad_fwd, bad_spring;
   size_t term_budget = size_t(1) << 31;  // bytes of backward scratch per group
+  // loss-chain slots: per-node loss terms + the chain's result. Slot 0 serves synchronous
+  // compute_loss calls; train_loop rotates through all of them so the chains of successive
+  // epochs run concurrently (they only feed the history rows and the error check).
+  struct ChainSlot {
+    DBuf<double> pt, dtm, out;
+    DBuf<int32_t> bad;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+    double* host = nullptr;  // pinned: {phys_sq, data_sq, first bad element (as double)}
+  };
+  std::deque<ChainSlot> slots;  // stable addresses as slots are added
+  double* slot_host = nullptr;
+  ~sc_trainer() {
+    for (ChainSlot& c : slots) {
+      if (c.st) cudaStreamSynchronize(c.st);
+      if (c.ev_in) cudaEventDestroy(c.ev_in);
+      if (c.ev_done) cudaEventDestroy(c.ev_done);
+      if (c.st) cudaStreamDestroy(c.st);
+    }
+    if (slot_host) cudaFreeHost(slot_host);
+  }
 };
 
 namespace {
@@ -691,24 +839,56 @@ struct Loss {
   double total = 0.0, physics = 0.0, data = 0.0;
 };
 
-// compute_loss (train.cpp:129-209); grads (53, for_each_gradient order) when non-null
-Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alpha,
-                  double* grads) {
-  const int B = static_cast<int>(bt.idx.size());
+constexpr size_t kMaxSlots = 32;
+
+sc_trainer::ChainSlot& chain_slot(sc_trainer* t, size_t k) {
+  while (t->slots.size() <= k) {
+    t->slots.emplace_back();
+    sc_trainer::ChainSlot& c = t->slots.back();
+    ck(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming), "event");
+    if (!t->slot_host)  // one pinned block for every slot's result (cudaHostAlloc is slow)
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&t->slot_host), kMaxSlots * 4 * sizeof(double),
+                       cudaHostAllocDefault),
+         "cudaHostAlloc");
+    c.host = t->slot_host + 4 * (t->slots.size() - 1);
+  }
+  return t->slots[k];
+}
+
+// What the host needs to finish a launched compute_loss.
+struct LossLaunch {
+  int B = 0;
+  unsigned long long cnt = 0;
+  int first_bad_fwd = kNone;  // first batch element with a non-finite cell impulse
+  int bad_node = 0;
+  int free_count = 0;
+  double phys_denom = 0.0;
+};
+
+// compute_loss (train.cpp:129-209), device part: the forward pass, the loss chain (async on the
+// slot's stream) and, when `grads` is given, the 53 gradient sums (returned synchronously).
+LossLaunch launch_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alpha,
+                       double* grads, sc_trainer::ChainSlot& slot) {
+  LossLaunch L;
+  const int B = L.B = static_cast<int>(bt.idx.size());
   if (B == 0) fail(SC_ERR_CONFIG, "compute_loss: empty batch");
   if (!(params.isru_alpha > 0.0)) fail(SC_ERR_CONFIG, "isru_alpha: must be > 0");
   const int64_t n = t->n;
   const size_t bn = static_cast<size_t>(B) * n;
-  t->pt.ensure(bn);
-  t->dtm.ensure(bn);
+  // the slot's previous chain must be done with its buffers
+  ck(cudaStreamWaitEvent(t->s0, slot.ev_done, 0), "wait");
+  slot.pt.ensure(bn);
+  slot.dtm.ensure(bn);
+  slot.out.ensure(2);
+  slot.bad.ensure(1);
   if (grads) {
     t->rp.ensure(bn * 3);
     t->rd.ensure(bn * 3);
   }
   t->count.ensure(1);
   t->bad_fwd.ensure(B);
-  t->bad_b.ensure(1);
-  t->chain_out.ensure(2);
   ck(cudaMemsetAsync(t->count.p, 0, sizeof(unsigned long long), t->s0), "memset");
   ck(cudaMemsetAsync(t->bad_fwd.p, 0x7F, sizeof(int32_t) * B, t->s0), "memset");
 
@@ -729,20 +909,24 @@ Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alph
   la.cloth = static_cast<const ClothConst<double>*>(t->view.cloths);
   la.rp = grads ? t->rp.p : nullptr;
   la.rd = grads ? t->rd.p : nullptr;
-  la.phys_term = t->pt.p;
-  la.data_term = t->dtm.p;
+  la.phys_term = slot.pt.p;
+  la.data_term = slot.dtm.p;
   la.data_count = t->count.p;
   la.bad_fwd = t->bad_fwd.p;
   loss_fwd_kernel<<<grid_for(static_cast<int64_t>(bn)), 256, 0, t->s0>>>(la);
   ck(cudaGetLastError(), "loss_fwd_kernel");
-  ck(cudaEventRecord(t->ev_fwd, t->s0), "event");
-  ck(cudaStreamWaitEvent(t->s1, t->ev_fwd, 0), "wait");
-  loss_chain_kernel<<<1, 32, 0, t->s1>>>(t->pt.p, t->dtm.p, B, n, t->chain_out.p, t->bad_b.p);
+  ck(cudaEventRecord(slot.ev_in, t->s0), "event");
+  ck(cudaStreamWaitEvent(slot.st, slot.ev_in, 0), "wait");
+  loss_chain_kernel<<<1, 256, 0, slot.st>>>(slot.pt.p, slot.dtm.p, B, n, slot.out.p, slot.bad.p);
   ck(cudaGetLastError(), "loss_chain_kernel");
-  ck(cudaEventRecord(t->ev_chain, t->s1), "event");
+  ck(cudaMemcpyAsync(slot.host, slot.out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, slot.st),
+     "D2H chain");
+  ck(cudaMemcpyAsync(slot.host + 3, slot.bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, slot.st),
+     "D2H chain");
+  ck(cudaEventRecord(slot.ev_done, slot.st), "event");
 
-  const int free_count = static_cast<int>(n) - t->n_pins;
-  const double phys_denom = 3.0 * static_cast<double>(B) * free_count;
+  L.free_count = static_cast<int>(n) - t->n_pins;
+  L.phys_denom = 3.0 * static_cast<double>(B) * L.free_count;
   if (grads) {
     t->grads.ensure(kScalars);
     ck(cudaMemsetAsync(t->grads.p, 0, sizeof(double) * kScalars, t->s0), "memset");
@@ -762,27 +946,21 @@ Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alph
       ba.upstream = nullptr;
       ba.rp = t->rp.p;
       ba.rd = t->rd.p;
-      ba.phys_coeff = free_count > 0 ? 2.0 * alpha / phys_denom : 0.0;
+      ba.phys_coeff = L.free_count > 0 ? 2.0 * alpha / L.phys_denom : 0.0;
       ba.alpha_loss = alpha;
       ba.data_count = t->count.p;
       ba.terms = t->terms.p;
       ba.chunks = chunks;
       bwd_terms_kernel<<<grid_for(n * nbat), 256, 0, t->s0>>>(ba);
       ck(cudaGetLastError(), "bwd_terms_kernel");
-      bwd_reduce_kernel<<<nbat * chunks, 64, 0, t->s0>>>(t->terms.p, n, chunks, t->partial.p);
+      bwd_reduce_kernel<<<nbat * chunks, 256, 0, t->s0>>>(t->terms.p, n, chunks, t->partial.p);
       ck(cudaGetLastError(), "bwd_reduce_kernel");
       bwd_final_kernel<<<1, 64, 0, t->s0>>>(t->partial.p, nbat, chunks, t->grads.p);
       ck(cudaGetLastError(), "bwd_final_kernel");
     }
   }
-  ck(cudaStreamWaitEvent(t->s0, t->ev_chain, 0), "join");
-  double chain[2];
-  int32_t bad_b = kNone;
-  unsigned long long cnt = 0;
   std::vector<int32_t> bad_fwd(static_cast<size_t>(B));
-  ck(cudaMemcpyAsync(chain, t->chain_out.p, sizeof chain, cudaMemcpyDeviceToHost, t->s0), "D2H");
-  ck(cudaMemcpyAsync(&bad_b, t->bad_b.p, sizeof bad_b, cudaMemcpyDeviceToHost, t->s0), "D2H");
-  ck(cudaMemcpyAsync(&cnt, t->count.p, sizeof cnt, cudaMemcpyDeviceToHost, t->s0), "D2H");
+  ck(cudaMemcpyAsync(&L.cnt, t->count.p, sizeof L.cnt, cudaMemcpyDeviceToHost, t->s0), "D2H");
   ck(cudaMemcpyAsync(bad_fwd.data(), t->bad_fwd.p, sizeof(int32_t) * B, cudaMemcpyDeviceToHost,
                      t->s0),
      "D2H");
@@ -791,27 +969,43 @@ Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alph
                        t->s0),
        "D2H");
   ck(cudaStreamSynchronize(t->s0), "compute_loss");
-  // the reference meets the errors in batch order: element b's forward_impulse throws before
-  // b's loss check (train.cpp:146-182)
-  int bf = kNone;
   for (int b = 0; b < B; ++b)
     if (bad_fwd[static_cast<size_t>(b)] != kNone) {
-      bf = b;
+      L.first_bad_fwd = b;
+      L.bad_node = bad_fwd[static_cast<size_t>(b)];
       break;
     }
-  if (bf != kNone && bf <= bad_b)
-    fail(SC_ERR_NUMERICS, diagnose_forward(t, bt.idx[static_cast<size_t>(bf)],
-                                           bad_fwd[static_cast<size_t>(bf)], params));
+  return L;
+}
+
+// compute_loss, host part: waits for the slot's chain, applies the reference's error order
+// (element b's forward_impulse throws before b's loss check, train.cpp:146-182) and forms the
+// loss values (train.cpp:185-189).
+Loss finish_loss(sc_trainer* t, const sc_params& params, const std::vector<int32_t>& idx,
+                 double alpha, const LossLaunch& L, sc_trainer::ChainSlot& slot) {
+  ck(cudaEventSynchronize(slot.ev_done), "loss chain");
+  const double ps = slot.host[0], ds = slot.host[1];
+  int32_t bad_b;
+  std::memcpy(&bad_b, slot.host + 3, sizeof bad_b);
+  if (L.first_bad_fwd != kNone && L.first_bad_fwd <= bad_b)
+    fail(SC_ERR_NUMERICS, diagnose_forward(t, idx[static_cast<size_t>(L.first_bad_fwd)],
+                                           L.bad_node, params));
   if (bad_b != kNone)
     fail(SC_ERR_NUMERICS, "non-finite loss at batch element " + std::to_string(bad_b) +
-                              " (frame " + std::to_string(bt.idx[static_cast<size_t>(bad_b)]) +
-                              ")");
+                              " (frame " + std::to_string(idx[static_cast<size_t>(bad_b)]) + ")");
   Loss loss;
-  const double data_denom = 6.0 * static_cast<double>(cnt);
-  loss.physics = free_count > 0 ? chain[0] / phys_denom : 0.0;
-  loss.data = cnt > 0 ? chain[1] / data_denom : 0.0;
+  const double data_denom = 6.0 * static_cast<double>(L.cnt);
+  loss.physics = L.free_count > 0 ? ps / L.phys_denom : 0.0;
+  loss.data = L.cnt > 0 ? ds / data_denom : 0.0;
   loss.total = alpha * loss.physics + (1.0 - alpha) * loss.data;
   return loss;
+}
+
+Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alpha,
+                  double* grads) {
+  sc_trainer::ChainSlot& slot = chain_slot(t, 0);
+  const LossLaunch L = launch_loss(t, params, bt, alpha, grads, slot);
+  return finish_loss(t, params, bt.idx, alpha, L, slot);
 }
 
 // ---- optimizer / schedule / DE / loop (train.cpp:54-63, 212-375) ----------------------------
@@ -1037,9 +1231,6 @@ sc_status sc_trainer_create(int device, const sc_scene_desc* scene, int32_t fram
                                   " has non-finite components");
       ck(cudaSetDevice(device), "cudaSetDevice");
       ck(cudaStreamCreateWithFlags(&t->s0, cudaStreamNonBlocking), "stream");
-      ck(cudaStreamCreateWithFlags(&t->s1, cudaStreamNonBlocking), "stream");
-      ck(cudaEventCreateWithFlags(&t->ev_fwd, cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&t->ev_chain, cudaEventDisableTiming), "event");
       t->fx.ensure(elems);
       t->fv.ensure(elems);
       ck(cudaMemcpy(t->fx.p, frames_x, elems * sizeof(double), cudaMemcpyHostToDevice), "H2D");
@@ -1056,11 +1247,7 @@ void sc_trainer_destroy(sc_trainer* t) {
   if (!t) return;
   if (t->ctx) cudaSetDevice(t->device);
   if (t->s0) cudaStreamSynchronize(t->s0);
-  if (t->s1) cudaStreamSynchronize(t->s1);
-  if (t->ev_fwd) cudaEventDestroy(t->ev_fwd);
-  if (t->ev_chain) cudaEventDestroy(t->ev_chain);
   if (t->s0) cudaStreamDestroy(t->s0);
-  if (t->s1) cudaStreamDestroy(t->s1);
   if (t->ctx) sc_ctx_destroy(t->ctx);
   delete t;
 }
@@ -1158,7 +1345,7 @@ sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double
     ba.chunks = chunks;
     bwd_terms_kernel<<<grid_for(n), 256>>>(ba);
     ck(cudaGetLastError(), "bwd_terms_kernel");
-    bwd_reduce_kernel<<<chunks, 64>>>(terms.p, n, chunks, partial.p);
+    bwd_reduce_kernel<<<chunks, 256>>>(terms.p, n, chunks, partial.p);
     ck(cudaGetLastError(), "bwd_reduce_kernel");
     bwd_final_kernel<<<1, 64>>>(partial.p, 1, chunks, grads.p);
     ck(cudaGetLastError(), "bwd_final_kernel");
@@ -1190,29 +1377,76 @@ sc_status sc_trainer_run(sc_trainer* t, const sc_train_config* cfg, const sc_par
     const int64_t start = opt.step;
     Batch batch;
     double grads[kScalars];
+    // epochs run back to back; each epoch's loss chain proceeds on its own slot while the next
+    // epochs compute, and is harvested in epoch order (history rows, error check) — the first
+    // failing epoch raises exactly what the reference raises there
+    struct Pending {
+      size_t slot;
+      int e;
+      int64_t step;
+      double lr;
+      sc_params p;
+      std::vector<int32_t> idx;
+      LossLaunch L;
+    };
+    std::vector<Pending> pend;
+    size_t head = 0;
+    const size_t slot_bytes =
+        static_cast<size_t>(cfg->batch_size) * static_cast<size_t>(t->n) * 2 * sizeof(double);
+    const size_t nslots = std::max<size_t>(
+        1, std::min<size_t>(kMaxSlots, (size_t(1) << 30) / std::max<size_t>(slot_bytes, 1)));
+    for (size_t k = 0; k < nslots; ++k) {  // every allocation before the epochs (cudaMalloc syncs)
+      sc_trainer::ChainSlot& c = chain_slot(t, k);
+      c.pt.ensure(slot_bytes / (2 * sizeof(double)));
+      c.dtm.ensure(slot_bytes / (2 * sizeof(double)));
+      c.out.ensure(2);
+      c.bad.ensure(1);
+    }
+    {
+      const size_t bn = static_cast<size_t>(cfg->batch_size) * static_cast<size_t>(t->n);
+      t->rp.ensure(bn * 3);
+      t->rd.ensure(bn * 3);
+      batch.idx_d.ensure(static_cast<size_t>(cfg->batch_size));
+      batch.force_dt.ensure(bn * 3);
+    }
+    auto harvest = [&](const Pending& q) {
+      Loss loss;
+      try {
+        loss = finish_loss(t, q.p, q.idx, cfg->alpha, q.L, t->slots[q.slot]);
+      } catch (const Fail& f) {
+        if (f.code != SC_ERR_NUMERICS) throw;
+        fail(SC_ERR_NUMERICS, f.msg + " [optimizer step " + std::to_string(q.step) + "]");
+      }
+      if (history_out) {
+        double* row = history_out + static_cast<int64_t>(q.e) * 5;
+        row[0] = static_cast<double>(q.step);
+        row[1] = q.lr;
+        row[2] = loss.physics;
+        row[3] = loss.data;
+        row[4] = loss.total;
+      }
+    };
     for (int e = 0; e < cfg->epochs; ++e) {
       const int64_t step = start + e;
       const double lr = schedule_lr(*cfg, static_cast<int>(step));
       Rng rng(Rng::mix(cfg->seed, static_cast<uint64_t>(step)));
       sample_batch(t, cfg->batch_size, rng, batch);
       batch_targets(t, batch);
-      Loss loss;
-      try {
-        loss = compute_loss(t, to_c(params), batch, cfg->alpha, grads);
-      } catch (const Fail& f) {
-        if (f.code != SC_ERR_NUMERICS) throw;
-        fail(SC_ERR_NUMERICS, f.msg + " [optimizer step " + std::to_string(step) + "]");
+      const size_t k = static_cast<size_t>(e) % nslots;
+      if (pend.size() - head == nslots) harvest(pend[head++]);  // frees slot k
+      Pending q{k, e, step, lr, to_c(params), batch.idx, LossLaunch{}};
+      q.L = launch_loss(t, q.p, batch, cfg->alpha, grads, chain_slot(t, k));
+      if (q.L.first_bad_fwd != kNone) {  // raises: earlier epochs' chains first, then this one
+        while (head < pend.size()) harvest(pend[head++]);
+        harvest(q);
       }
       adam_update(params, grads, opt, lr);
-      if (history_out) {
-        double* row = history_out + static_cast<int64_t>(e) * 5;
-        row[0] = static_cast<double>(step);
-        row[1] = lr;
-        row[2] = loss.physics;
-        row[3] = loss.data;
-        row[4] = loss.total;
-      }
+      pend.push_back(std::move(q));
+      while (head < pend.size() &&
+             cudaEventQuery(t->slots[pend[head].slot].ev_done) == cudaSuccess)
+        harvest(pend[head++]);
     }
+    while (head < pend.size()) harvest(pend[head++]);
     *params_out = to_c(params);
     if (trainable_out)
       for (int g = 0; g < 7; ++g) trainable_out[g] = params.trainable[static_cast<size_t>(g)] ? 1 : 0;
