@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstencilcloth_b200.so")
+LIB_PATH = os.environ.get("SC_B200_LIB") or os.path.join(_HERE, "libstencilcloth_b200.so")
 
 SC_OK, SC_ERR_CONFIG, SC_ERR_NUMERICS, SC_ERR_CUDA, SC_ERR_STATE = 0, 1, 2, 3, 4
 SC_F32, SC_F64 = 0, 1

@@ -12,6 +12,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -274,6 +275,8 @@ void upload_scene(sc_ctx* c, const sc_scene_desc* s) {
     k.plug_pressure = (d.plug_pressure && k.pressure != T(0)) ? 1 : 0;
     k.plug_gravity = d.plug_gravity ? 1 : 0;
     k.plug_drag = d.plug_drag ? 1 : 0;
+    for (int q = 0; q < 3; ++q) k.fin[q] = k.plug_gravity ? k.dv[q] : T(0);
+    k.fin[3] = k.plug_drag ? k.drag_c : T(0);
     k.n_spheres = d.n_spheres;
     k.sphere0 = static_cast<int32_t>(sph.size());
     for (int q = 0; q < d.n_spheres; ++q) {

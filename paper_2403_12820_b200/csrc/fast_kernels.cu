@@ -180,15 +180,17 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
                                           const float* v2p, int lane, float mL, float mRt,
                                           float m1, float m2, V (&A0)[4], V (&A1)[4], V (&A2)[4],
                                           V bias) {
+  // windows are loaded right before their edge groups (rows R, R-2, R-1 in that order) so the
+  // live register set stays small: R's window, then at most one of R-2 / R-1 beside it
   V xr[8], vr[8], x1[8], v1[8], x2[4], v2[4];
   win8(xR, lane, xr);
   win8(vR, lane, vr);
-  win8(x1p, lane, x1);
-  win8(v1p, lane, v1);
-  win4(x2p, lane, x2);
-  win4(v2p, lane, v2);
   V dummy{};
   if (TAIL) {
+    win8(x1p, lane, x1);
+    win8(v1p, lane, v1);
+    win4(x2p, lane, x2);
+    win4(v2p, lane, v2);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       edge<ALPHA1, true, false>(f, 1, 3, vsub(x1[k + 2], xr[k + 2]), vsub(v1[k + 2], vr[k + 2]),
@@ -246,7 +248,21 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     else if (e >= 4) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[e - 2], dummy);
     else edge<ALPHA1, true, true>(f, 8, 10, dx, dv, A2[e - 2], A2[e]);
   }
-  // N edges (R-1 -> R) and N2 edges (R-2 -> R), owned columns
+  // N2 edges (R-2 -> R), owned columns
+  win4(x2p, lane, x2);
+  win4(v2p, lane, v2);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    V dx2 = vsub(x2[k], xr[k + 2]), dv2 = vsub(v2[k], vr[k + 2]);
+    if (GENERAL) {
+      dx2 = vscale(dx2, m2);
+      dv2 = vscale(dv2, m2);
+    }
+    edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[k], A2[k]);
+  }
+  // N edges (R-1 -> R), owned columns
+  win8(x1p, lane, x1);
+  win8(v1p, lane, v1);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     V dx = vsub(x1[k + 2], xr[k + 2]), dv = vsub(v1[k + 2], vr[k + 2]);
@@ -255,12 +271,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
       dv = vscale(dv, m1);
     }
     edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[k], A2[k]);
-    V dx2 = vsub(x2[k], xr[k + 2]), dv2 = vsub(v2[k], vr[k + 2]);
-    if (GENERAL) {
-      dx2 = vscale(dx2, m2);
-      dv2 = vscale(dv2, m2);
-    }
-    edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[k], A2[k]);
   }
   // NE edges: a = (ix0-1+e, R-1) (j = e+1), b = (ix0+e, R) (j = e+2)
 #pragma unroll
@@ -290,18 +300,164 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   }
 }
 
+// z component of column k (0..3) of a pair-packed accumulator row
+__device__ __forceinline__ float& zc(float2 (&a)[2], int k) { return (k & 1) ? a[k >> 1].y : a[k >> 1].x; }
+
+// z windows as register pairs: columns ix0-2 .. ix0+5 (w8) and ix0 .. ix0+3 (w4)
+__device__ __forceinline__ void win8p(const float* zplane, int lane, float2* o) {
+  o[0] = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
+  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+  o[1] = make_float2(m.x, m.y);
+  o[2] = make_float2(m.z, m.w);
+  o[3] = *reinterpret_cast<const float2*>(zplane + FW * lane + 8);
+}
+__device__ __forceinline__ void win4p(const float* zplane, int lane, float2* o) {
+  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+  o[0] = make_float2(m.x, m.y);
+  o[1] = make_float2(m.z, m.w);
+}
+__device__ __forceinline__ float zw(const float2* w, int i) { return (i & 1) ? w[i >> 1].y : w[i >> 1].x; }
+
+// comp_pass for z with adjacent columns packed where the edge geometry keeps register pairs
+// aligned: E2 edges (offset 2) and the vertical N / N2 edges run two columns per FFMA2 / MUFU
+// pair; E, NE, NW (odd offsets) stay scalar on the pair halves.
+template <bool ALPHA1, bool GENERAL, bool TAIL>
+__device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, const float* vR,
+                                            const float* x1p, const float* v1p, const float* x2p,
+                                            const float* v2p, int lane, float mL, float mRt,
+                                            float m1, float m2, float2 (&A0)[2], float2 (&A1)[2],
+                                            float2 (&A2)[2], float bias) {
+  float2 xr[4], vr[4], x1[4], v1[4], x2[2], v2[2];
+  win8p(xR, lane, xr);
+  win8p(vR, lane, vr);
+  float dummy = 0.f;
+  float2 dummy2{};
+  if (TAIL) {
+    win8p(x1p, lane, x1);
+    win8p(v1p, lane, v1);
+    win4p(x2p, lane, x2);
+    win4p(v2p, lane, v2);
+    // N / N2 a-sides (packed), NE / NW a-sides (scalar)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      edge<ALPHA1, true, false>(f, 1, 3, vsub(x1[j + 1], xr[j + 1]), vsub(v1[j + 1], vr[j + 1]),
+                                A1[j], dummy2);
+      edge<ALPHA1, true, false>(f, 9, 11, vsub(x2[j], xr[j + 1]), vsub(v2[j], vr[j + 1]), A0[j],
+                                dummy2);
+    }
+#pragma unroll
+    for (int e = 1; e < 5; ++e) {
+      float dx = zw(x1, e + 1) - zw(xr, e + 2), dv = zw(v1, e + 1) - zw(vr, e + 2);
+      if (e == 4) {
+        dx *= mRt;
+        dv *= mRt;
+      }
+      edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, e - 1), dummy);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float dx = zw(x1, e + 2) - zw(xr, e + 1), dv = zw(v1, e + 2) - zw(vr, e + 1);
+      if (e == 0) {
+        dx *= mL;
+        dv *= mL;
+      }
+      edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, e), dummy);
+    }
+    return;
+  }
+  // init row R: b + v*wV
+#pragma unroll
+  for (int j = 0; j < 2; ++j) A2[j] = vfma(vr[j + 1], f.wv, make_float2(bias, bias));
+
+  // E edges in row R (scalar): a = col ix0-1+e, b = col ix0+e
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = zw(xr, e + 1) - zw(xr, e + 2), dv = zw(vr, e + 1) - zw(vr, e + 2);
+    if (e == 0 || e == 4) {
+      const float m = e == 0 ? mL : mRt;
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, zc(A2, 0));
+    else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, zc(A2, 3), dummy);
+    else edge<ALPHA1, true, true>(f, 0, 2, dx, dv, zc(A2, e - 1), zc(A2, e));
+  }
+  // E2 edges in row R, packed: pair j = edges e = 2j, 2j+1 (a = cols ix0-2+e, b = ix0+e)
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    float2 dx = vsub(xr[j], xr[j + 1]), dv = vsub(vr[j], vr[j + 1]);
+    if (j == 0 || j == 2) {
+      const float m = j == 0 ? mL : mRt;
+      dx = vscale(dx, m);
+      dv = vscale(dv, m);
+    }
+    if (j == 0) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy2, A2[0]);
+    else if (j == 2) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[1], dummy2);
+    else edge<ALPHA1, true, true>(f, 8, 10, dx, dv, A2[0], A2[1]);
+  }
+  // N2 edges (R-2 -> R), then N edges (R-1 -> R), packed column pairs
+  win4p(x2p, lane, x2);
+  win4p(v2p, lane, v2);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    float2 dx2 = vsub(x2[j], xr[j + 1]), dv2 = vsub(v2[j], vr[j + 1]);
+    if (GENERAL) {
+      dx2 = vscale(dx2, m2);
+      dv2 = vscale(dv2, m2);
+    }
+    edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[j], A2[j]);
+  }
+  win8p(x1p, lane, x1);
+  win8p(v1p, lane, v1);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    float2 dx = vsub(x1[j + 1], xr[j + 1]), dv = vsub(v1[j + 1], vr[j + 1]);
+    if (GENERAL) {
+      dx = vscale(dx, m1);
+      dv = vscale(dv, m1);
+    }
+    edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[j], A2[j]);
+  }
+  // NE edges (scalar): a = (ix0-1+e, R-1), b = (ix0+e, R)
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = zw(x1, e + 1) - zw(xr, e + 2), dv = zw(v1, e + 1) - zw(vr, e + 2);
+    if (GENERAL || e == 0 || e == 4) {
+      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, zc(A2, 0));
+    else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, 3), dummy);
+    else edge<ALPHA1, true, true>(f, 4, 6, dx, dv, zc(A1, e - 1), zc(A2, e));
+  }
+  // NW edges (scalar): a = (ix0+e, R-1), b = (ix0+e-1, R)
+#pragma unroll
+  for (int e = 0; e < 5; ++e) {
+    float dx = zw(x1, e + 2) - zw(xr, e + 1), dv = zw(v1, e + 2) - zw(vr, e + 1);
+    if (GENERAL || e == 0 || e == 4) {
+      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
+      dx *= m;
+      dv *= m;
+    }
+    if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, 0), dummy);
+    else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, zc(A2, 3));
+    else edge<ALPHA1, true, true>(f, 5, 7, dx, dv, zc(A1, e), zc(A2, e - 1));
+  }
+}
+
 template <bool ALPHA1, bool GENERAL, bool TAIL>
 __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, const float* row1,
                                          const float* row2, int lane, float mL, float mRt,
                                          float m1, float m2, float2 (&P0)[4], float2 (&P1)[4],
-                                         float2 (&P2)[4], float (&Z0)[4], float (&Z1)[4],
-                                         float (&Z2)[4]) {
+                                         float2 (&P2)[4], float2 (&Z0)[2], float2 (&Z1)[2],
+                                         float2 (&Z2)[2]) {
   comp_pass<ALPHA1, GENERAL, TAIL, float2>(f, rowR + XY_X, rowR + XY_V, row1 + XY_X, row1 + XY_V,
                                            row2 + XY_X, row2 + XY_V, lane, mL, mRt, m1, m2, P0,
                                            P1, P2, make_float2(f.b[0], f.b[1]));
-  comp_pass<ALPHA1, GENERAL, TAIL, float>(f, rowR + Z_X, rowR + Z_V, row1 + Z_X, row1 + Z_V,
-                                          row2 + Z_X, row2 + Z_V, lane, mL, mRt, m1, m2, Z0, Z1,
-                                          Z2, f.b[2]);
+  comp_pass_z<ALPHA1, GENERAL, TAIL>(f, rowR + Z_X, rowR + Z_V, row1 + Z_X, row1 + Z_V,
+                                     row2 + Z_X, row2 + Z_V, lane, mL, mRt, m1, m2, Z0, Z1, Z2,
+                                     f.b[2]);
 }
 
 // component d of x (X = true) or v at box column j of a ring slot
@@ -327,26 +483,40 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   const int r_first = y0 - 2;
   const int r_last = y1 + 1;
 
-  auto issue = [&](int row) {  // lane 0 only
-    const int t = row - r_first;
-    uint64_t* bar = &full[t % RING];
-    float* slot = ring + (t % RING) * ROWF;
-    mbar_expect_tx(bar, ROW_BYTES);
-    tma_load_4d(slot, tmap_xy, x0 - 4, row - a.g0, 0, b, bar);
-    tma_load_4d(slot + Z_X, tmap_z, x0 - 4, row - a.g0, 0, b, bar);
+  // ring slot t % RING of row r_first + t is tracked incrementally (no modulo in the loop); the
+  // TMA operands are formed outside the lane-0 branch so they stay warp-uniform
+  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full);
+  const int cx = x0 - 4, crow0 = r_first - a.g0;
+  auto issue = [&](int t, int sl) {  // row r_first + t into slot sl
+    const uint32_t dst = ring_s + static_cast<uint32_t>(sl) * (ROWF * 4);
+    const uint32_t bar = full_s + static_cast<uint32_t>(sl) * 8;
+    const int crow = crow0 + t;
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "n"(ROW_BYTES)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(tmap_xy)), "r"(cx), "r"(crow), "r"(0), "r"(b), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + Z_X * 4),
+          "l"(reinterpret_cast<uint64_t>(tmap_z)), "r"(cx), "r"(crow), "r"(0), "r"(b), "r"(bar)
+          : "memory");
+    }
   };
-  auto wait_slot = [&](int t) {
-    const int sl = t % RING;
+  auto wait_slot = [&](int sl) {
     mbar_wait(&full[sl], (phase >> sl) & 1u);
     phase ^= 1u << sl;
   };
+  auto nxt = [](int sl) { return sl + 1 == RING ? 0 : sl + 1; };
   __syncwarp();  // earlier generic reads of the ring are done before TMA refills it
-  if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue(r_first);
-    issue(r_first + 1);
-    issue(r_first + 2);
-  }
+  issue(0, 0);
+  issue(1, 1);
+  issue(2, 2);
   wait_slot(0);
   wait_slot(1);
 
@@ -359,35 +529,36 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
-  const int64_t S = a.plane_stride;
-  float* out_b = a.out + static_cast<int64_t>(b) * 6 * S;
   const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
-  const float dv_eff[3] = {cc.plug_gravity ? cc.dv[0] : 0.f, cc.plug_gravity ? cc.dv[1] : 0.f,
-                           cc.plug_gravity ? cc.dv[2] : 0.f};
-  const float drag_eff = cc.plug_drag ? cc.drag_c : 0.f;
+  const float dv_eff[3] = {cc.fin[0], cc.fin[1], cc.fin[2]};  // plugged gravity impulse or 0
+  const float drag_eff = cc.fin[3];                            // plugged drag coefficient or 0
 
   // accumulators [column] for rows R-2 (P0/Z0), R-1 (P1/Z1), R (P2/Z2): P = (x,y), Z = z
   float2 P0[4], P1[4], P2[4];
-  float Z0[4], Z1[4], Z2[4];
+  float2 Z0[2], Z1[2], Z2[2];  // column pairs (0,1), (2,3)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    P0[k] = P1[k] = P2[k] = make_float2(0.f, 0.f);
-    Z0[k] = Z1[k] = Z2[k] = 0.f;
-  }
+  for (int k = 0; k < 4; ++k) P0[k] = P1[k] = P2[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) Z0[j] = Z1[j] = Z2[j] = make_float2(0.f, 0.f);
+
+  // slots of rows R, R-1, R-2 (R-3 for the pressure finish) and of the prefetched row R+1
+  int sR = 2 % RING, s1 = 1, s2 = 0, s3 = RING - 1, sI = 3 % RING;
+  // output row pointers (x.xy plane and x.z plane) of the finished row R-2, advanced per row
+  const int64_t S = a.plane_stride;
+  float* const out_b = a.out + static_cast<int64_t>(b) * 6 * S;
+  float* oxy = out_b + 2 * (static_cast<int64_t>(y0 - 2 - a.g0) * a.pitch + ix0);
+  float* oz = out_b + 4 * S + static_cast<int64_t>(y0 - 2 - a.g0) * a.pitch + ix0;
 
 #pragma unroll 1
   for (int R = y0; R <= r_last; ++R) {
     const int t = R - r_first;
     __syncwarp();
-    if (lane == 0 && R + 1 <= r_last) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(R + 1);
-    }
-    wait_slot(t);
+    if (R + 1 <= r_last) issue(t + 1, sI);
+    wait_slot(sR);
 
-    const float* rowR = ring + (t % RING) * ROWF;
-    const float* row1 = ring + ((t + RING - 1) % RING) * ROWF;
-    const float* row2 = ring + ((t + RING - 2) % RING) * ROWF;
+    const float* rowR = ring + sR * ROWF;
+    const float* row1 = ring + s1 * ROWF;
+    const float* row2 = ring + s2 * ROWF;
     if (R >= y1) {
       if (R < ny)
         row_pass<ALPHA1, false, true>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2,
@@ -411,23 +582,24 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         win4(row2 + XY_V, lane, vs);
         win4(row2 + Z_X, lane, xz);
         win4(row2 + Z_V, lane, vz);
-        // add_plug_impulse gravity/drag + advance without colliders, IEEE-exact like PARITY
+        // add_plug_impulse gravity/drag + advance without colliders (no mask, no contact
+        // decision depends on it): FMA-contracted and x,y packed — part of FAST mode's 1e-5 bar
         float xo[3][4], vo[3][4];
+        const float2 dvxy = make_float2(dv_eff[0], dv_eff[1]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float xin[3] = {xs[k].x, xs[k].y, xz[k]};
-          const float vin[3] = {vs[k].x, vs[k].y, vz[k]};
-          const float acc[3] = {P0[k].x, P0[k].y, Z0[k]};
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            // unplugged gravity / drag enter as +0 terms (branch-free; only the sign of an
-            // exactly-zero impulse can differ from skipping them)
-            float imp = __fadd_rn(acc[d], dv_eff[d]);
-            imp = __fsub_rn(imp, __fmul_rn(vin[d], drag_eff));
-            const float vv = __fadd_rn(vin[d], imp);
-            vo[d][k] = vv;
-            xo[d][k] = __fadd_rn(xin[d], __fmul_rn(vv, cc.dt));
-          }
+          float2 imp = __fadd2_rn(P0[k], dvxy);
+          imp = __ffma2_rn(vs[k], make_float2(-drag_eff, -drag_eff), imp);
+          const float2 vv = __fadd2_rn(vs[k], imp);
+          const float2 xx = __ffma2_rn(vv, make_float2(cc.dt, cc.dt), xs[k]);
+          const float iz = fmaf(vz[k], -drag_eff, zc(Z0, k) + dv_eff[2]);
+          const float vvz = vz[k] + iz;
+          vo[0][k] = vv.x;
+          vo[1][k] = vv.y;
+          vo[2][k] = vvz;
+          xo[0][k] = xx.x;
+          xo[1][k] = xx.y;
+          xo[2][k] = fmaf(vvz, cc.dt, xz[k]);
         }
         if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
 #pragma unroll
@@ -451,13 +623,13 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           bool fin_imp = true, fin = true;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            fin_imp = fin_imp && isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(Z0[k]);
+            fin_imp = fin_imp && isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(zc(Z0, k));
 #pragma unroll
             for (int d = 0; d < 3; ++d) fin = fin && isfinite(xo[d][k]) && isfinite(vo[d][k]);
           }
           if (!fin_imp) {
             for (int k = 0; k < 4; ++k)
-              if (!(isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(Z0[k]))) {
+              if (!(isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(zc(Z0, k)))) {
                 const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
                                                static_cast<unsigned long long>(Rf * nx + ix0 + k);
                 atomicMin(&a.health[b].impulse_key, key);
@@ -466,24 +638,21 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           }
           if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
         }
-        float* oxy = out_b + 2 * (lr * a.pitch + ix0);
-        float* ovxy = out_b + 2 * S + 2 * (lr * a.pitch + ix0);
+        float* ovxy = oxy + 2 * S;
         reinterpret_cast<float4*>(oxy)[0] = make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
         reinterpret_cast<float4*>(oxy)[1] = make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
         reinterpret_cast<float4*>(ovxy)[0] = make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
         reinterpret_cast<float4*>(ovxy)[1] = make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
-        *reinterpret_cast<float4*>(out_b + 4 * S + lr * a.pitch + ix0) =
-            make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
-        *reinterpret_cast<float4*>(out_b + 5 * S + lr * a.pitch + ix0) =
-            make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
+        *reinterpret_cast<float4*>(oz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
+        *reinterpret_cast<float4*>(oz + S) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
       } else {
         // colliders / pressure / mask: one node at a time (compact code, same IEEE-exact chain)
-        const float* rs = ring + ((t + RING - 3) % RING) * ROWF;  // row Rf-1
+        const float* rs = ring + s3 * ROWF;  // row Rf-1
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           scratch[lane][k] = P0[k].x;  // own row of the scratch only: no cross-lane sync
           scratch[lane][4 + k] = P0[k].y;
-          scratch[lane][8 + k] = Z0[k];
+          scratch[lane][8 + k] = zc(Z0, k);
         }
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
@@ -529,18 +698,28 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         }
       }
     }
-    // rotate accumulator rows
+    // advance: slots, output rows, accumulator rows
+    s3 = s2;
+    s2 = s1;
+    s1 = sR;
+    sR = sI;
+    sI = nxt(sI);
+    oxy += 2 * a.pitch;
+    oz += a.pitch;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      Z0[j] = Z1[j];
+      Z1[j] = Z2[j];
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       P0[k] = P1[k];
       P1[k] = P2[k];
-      Z0[k] = Z1[k];
-      Z1[k] = Z2[k];
     }
   }
 }
 
-__device__ unsigned long long* g_unit_times = nullptr;  // debug: [units][2] globaltimer
+__device__ unsigned long long* g_unit_times = nullptr;  // debug: [units][3] start, end, sm/warp
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -559,8 +738,11 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
   y1 = u0 + static_cast<int>((static_cast<int64_t>(seg + 1) * rows) / n_segs);
 }
 
+#ifndef SC_FAST_MINB
+#define SC_FAST_MINB 16
+#endif
 template <bool ALPHA1, int RING>
-__global__ void __launch_bounds__(32, 16) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
+__global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
@@ -584,10 +766,16 @@ __global__ void __launch_bounds__(32, 16) fast_step_kernel(const __grid_constant
   asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t phase = 0;
   unsigned long long* times = g_unit_times;
-  if (times && threadIdx.x == 0) times[2 * unit] = gtimer();
+  if (times && threadIdx.x == 0) {
+    unsigned smid, wid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    times[3 * unit] = gtimer();
+    times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
+  }
   if (y0 < y1)
     run_unit<ALPHA1, RING>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch, phase);
-  if (times && threadIdx.x == 0) times[2 * unit + 1] = gtimer();
+  if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
   // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -609,7 +797,10 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // global memory). That covers both the read-after-write (halo rows of step k-1) and the
 // write-after-read (neighbours done reading the buffer this step overwrites) hazards.
 template <bool ALPHA1, int RING>
-__global__ void __launch_bounds__(32, 12) fast_multi_kernel(
+#ifndef SC_MULTI_MINB
+#define SC_MULTI_MINB 12
+#endif
+__global__ void __launch_bounds__(32, SC_MULTI_MINB) fast_multi_kernel(
     const __grid_constant__ CUtensorMap txy0, const __grid_constant__ CUtensorMap tz0,
     const __grid_constant__ CUtensorMap txy1, const __grid_constant__ CUtensorMap tz1,
     const StepArgs<float> a0, const FastNet f, const int n_strips, const int seg_rows,

@@ -78,6 +78,8 @@ struct NetConst {
 // host with the same single IEEE operation (so they are bit-identical).
 template <typename T>
 struct ClothConst {
+  // FAST simple finish: plugged gravity impulse (or 0) x3, plugged drag coefficient (or 0)
+  T fin[4];
   T dt;
   T scale;     // dt / mass                          (kernels.hpp:182)
   T drag_c;    // drag * scale                       (kernels.hpp:193)
