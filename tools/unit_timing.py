@@ -60,3 +60,8 @@ for c in sorted(set(cnt[key])):
 sm_mean = np.array([d_us[sm == i].mean() for i in range(sm.max() + 1) if (sm == i).any()])
 print("per-SM mean duration: min %.1f p50 %.1f max %.1f" % (sm_mean.min(), np.median(sm_mean), sm_mean.max()))
 print("within-SM spread (max-min) median %.1f us" % np.median([d_us[sm == i].max() - d_us[sm == i].min() for i in range(sm.max() + 1) if (sm == i).any()]))
+# duration vs launch order (blockIdx): warps launched earlier get issue priority
+order = np.arange(len(d_us))
+rank = order * 16 // len(d_us)
+print("mean duration by launch-order sixteenth:", [round(float(d_us[rank == r].mean()), 1) for r in range(16)])
+np.save("gpurun_out/unit_timing_%d.npy" % cid, np.stack([t[:, 0], t[:, 1], sm, warp]))
