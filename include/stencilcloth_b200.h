@@ -252,11 +252,12 @@ sc_status sc_trainer_compute_loss(sc_trainer* trainer, const sc_params* params, 
                                   double* loss_out, double* grads_out);
 /* train_loop (train.cpp:343-375): DE pre-search + Adam epochs, or fine-tune from resume_params
  * (+ trainable flags, + the Adam state in opt_inout). history_out: epochs x {step, lr, physics,
- * data, total} (nullable); opt_inout (nullable) receives the final Adam state. */
+ * data, total} (nullable); opt_inout (nullable) receives the final Adam state; brackets_out
+ * (nullable, 14 doubles): the InitBracket {lo, hi} of each ParamGroup (net.hpp:28-31). */
 sc_status sc_trainer_run(sc_trainer* trainer, const sc_train_config* cfg,
                          const sc_params* resume_params, const uint8_t* resume_trainable,
                          sc_adam_state* opt_inout, sc_params* params_out, uint8_t* trainable_out,
-                         double* history_out);
+                         double* history_out, double* brackets_out);
 /* backward_gradients (net.cpp:144-201) for one state and upstream cotangent [node][3]. */
 sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double* x,
                                 const double* v, const sc_params* params, const double* upstream,

@@ -154,7 +154,7 @@ class Reference:
         L.ref_compute_loss.argtypes = [_I, _I, _CD, _I, _P, _P, _I, C.c_uint64, _PR, C.c_double,
                                        _I, _P, _P]
         L.ref_backward_gradients.argtypes = [_I, _I, _P, _P, _PR, _P, _P]
-        L.ref_train.argtypes = [_I, _I, _CD, _I, _P, _P, _TC, _PR, _P, _P]
+        L.ref_train.argtypes = [_I, _I, _CD, _I, _P, _P, _TC, _PR, _P, _P, _P]
 
     def _ck(self, rc):
         if rc != 0:
@@ -303,6 +303,8 @@ class Reference:
         out = _abi.sc_params()
         tr = np.zeros(7, np.uint8)
         hist = np.zeros((cfg.epochs, 5))
+        br = np.zeros(14)
         self._ck(self.lib.ref_train(nx, ny, C.byref(cloth), fx.shape[0], _p(fx), _p(fv),
-                                    C.byref(cfg), C.byref(out), _p(tr), _p(hist)))
+                                    C.byref(cfg), C.byref(out), _p(tr), _p(hist), _p(br)))
+        self.last_brackets = br
         return out, tr, hist

@@ -498,7 +498,7 @@ int ref_backward_gradients(int nx, int ny, const double* x, const double* v, con
 
 int ref_train(int nx, int ny, const sc_cloth_desc* cd, int frames, const double* fx,
               const double* fv, const sc_train_config* c, sc_params* params_out,
-              uint8_t* trainable_out, double* history_out) {
+              uint8_t* trainable_out, double* history_out, double* brackets_out) {
   return guarded([&] {
     const Scene scene = to_scene(nx, ny, cd, fx, fv);
     const Trajectory traj = make_traj(nx, ny, cd, frames, fx, fv);
@@ -536,8 +536,13 @@ int ref_train(int nx, int ny, const sc_cloth_desc* cd, int frames, const double*
     for (int d = 0; d < 3; ++d) params_out->linear_b[d] = flat[24 + d];
     params_out->self_velocity_w = flat[51];
     params_out->isru_alpha = flat[52];
-    for (int g = 0; g < kParamGroups; ++g)
+    for (int g = 0; g < kParamGroups; ++g) {
       if (trainable_out) trainable_out[g] = q.is_trainable(static_cast<ParamGroup>(g)) ? 1 : 0;
+      if (brackets_out) {
+        brackets_out[2 * g] = q.brackets[static_cast<size_t>(g)].lo;
+        brackets_out[2 * g + 1] = q.brackets[static_cast<size_t>(g)].hi;
+      }
+    }
     if (history_out)
       for (size_t e = 0; e < r.history.size(); ++e) {
         history_out[5 * e] = r.history[e].step;

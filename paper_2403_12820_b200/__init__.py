@@ -22,8 +22,9 @@ from .training import (AdamState, DeConfig, LossRow, LossValue, ParamGradients, 
                     ScheduleConfig, ScheduleKind, TrainConfig, Trainer, TrainResult,
                     backward_gradients, gradient_check, sample_indices, train,
                        train_loop)
-from .trajio import (EvalReport, evaluate, export_obj, load_trajectory,  # noqa: E402
-                     save_trajectory, write_eval_csv)
+from .trajio import (Checkpoint, EvalReport, evaluate, export_obj, load_checkpoint,  # noqa: E402
+                     load_trajectory, save_checkpoint, save_trajectory, write_eval_csv,
+                     write_loss_csv)
 
 __all__ = [
     "BenchResult", "BoundarySpec", "ClothBatch", "ConfigError", "Context", "CudaError",
@@ -33,7 +34,8 @@ __all__ = [
     "load_scene", "nn_step", "params_fingerprint", "parse_scene", "plug_impulse", "rollout",
     "benchmark_sim", "simulate", "step_semi_implicit", "total_impulse",
     "EvalReport", "evaluate", "export_obj", "load_trajectory", "pinned_empty", "save_trajectory",
-    "write_eval_csv", "AdamState", "DeConfig", "LossRow", "LossValue", "ParamGradients",
+    "write_eval_csv", "Checkpoint", "load_checkpoint", "save_checkpoint", "write_loss_csv",
+    "AdamState", "DeConfig", "LossRow", "LossValue", "ParamGradients",
     "ScheduleConfig", "ScheduleKind", "TrainConfig", "Trainer", "TrainResult",
     "backward_gradients", "gradient_check", "sample_indices", "train", "train_loop",
 ]

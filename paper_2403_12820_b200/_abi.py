@@ -136,7 +136,7 @@ SIGNATURES = {
     "sc_sample_indices": (C.c_int, [_I, _I, C.c_uint64, _P]),
     "sc_trainer_compute_loss": (C.c_int, [_P, C.POINTER(sc_params), C.c_double, _P, _P]),
     "sc_trainer_run": (C.c_int, [_P, C.POINTER(sc_train_config), C.POINTER(sc_params), _P,
-                                 C.POINTER(sc_adam_state), C.POINTER(sc_params), _P, _P]),
+                                 C.POINTER(sc_adam_state), C.POINTER(sc_params), _P, _P, _P]),
     "sc_backward_gradients": (C.c_int, [C.c_int, _I, _I, _P, _P, C.POINTER(sc_params), _P, _P]),
     "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),

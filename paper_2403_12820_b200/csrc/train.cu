@@ -645,7 +645,12 @@ struct Rng {
 struct Params {
   std::array<double, kScalars> s{};
   std::array<bool, 7> trainable{};
+  std::array<double, 14> brackets{};  // InitBracket lo, hi per group (net.hpp:28-31)
   Params() {
+    for (int g = 0; g < 7; ++g) {
+      brackets[2 * g] = -1.0;
+      brackets[2 * g + 1] = 1.0;
+    }
     for (int c = 0; c < 12; ++c) s[c] = 1.0;  // kernel gains
     s[52] = 1.0;                              // alpha
     trainable.fill(true);
@@ -1182,6 +1187,10 @@ Params de_preprocess(sc_trainer* t, const sc_train_config& cfg, Rng& rng) {
   Br ab = bracket(best.alpha);
   ab.lo = std::max(ab.lo, 1e-3);
   br[6] = ab;
+  for (int g = 0; g < 7; ++g) {
+    params.brackets[2 * g] = br[static_cast<size_t>(g)].lo;
+    params.brackets[2 * g + 1] = br[static_cast<size_t>(g)].hi;
+  }
   params.s[52] = best.alpha;
   for (int s = 0; s < kScalars; ++s) {
     const int g = group_of(s);
@@ -1355,7 +1364,8 @@ sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double
 
 sc_status sc_trainer_run(sc_trainer* t, const sc_train_config* cfg, const sc_params* resume_params,
                          const uint8_t* resume_trainable, sc_adam_state* opt_inout,
-                         sc_params* params_out, uint8_t* trainable_out, double* history_out) {
+                         sc_params* params_out, uint8_t* trainable_out, double* history_out,
+                         double* brackets_out) {
   return guarded([&] {
     if (!t) fail(SC_ERR_STATE, "null trainer");
     if (!cfg || !params_out) fail(SC_ERR_CONFIG, "train: null argument");
@@ -1450,6 +1460,8 @@ sc_status sc_trainer_run(sc_trainer* t, const sc_train_config* cfg, const sc_par
     *params_out = to_c(params);
     if (trainable_out)
       for (int g = 0; g < 7; ++g) trainable_out[g] = params.trainable[static_cast<size_t>(g)] ? 1 : 0;
+    if (brackets_out)
+      for (int k = 0; k < 14; ++k) brackets_out[k] = params.brackets[static_cast<size_t>(k)];
     if (opt_inout) *opt_inout = opt;
   });
 }

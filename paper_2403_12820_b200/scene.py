@@ -87,6 +87,8 @@ class NetworkParams:
         self.trainable = [True] * 7
         self.trainable[ParamGroup.Kernel] = False
         self.trainable[ParamGroup.Alpha] = False
+        # InitBracket per group (net.hpp:28-31), set by the DE pre-search (train.cpp:296-310)
+        self.brackets = [(-1.0, 1.0)] * 7
 
     def scalars(self) -> List[float]:
         """for_each_scalar order (net.hpp:72-81)."""
@@ -127,7 +129,16 @@ class NetworkParams:
         return c
 
     def copy(self) -> "NetworkParams":
-        return NetworkParams.from_scalars(self.scalars())
+        p = NetworkParams.from_scalars(self.scalars())
+        p.trainable = list(self.trainable)
+        p.brackets = list(self.brackets)
+        return p
+
+    def is_trainable(self, g: "ParamGroup") -> bool:
+        return bool(self.trainable[int(g)])
+
+    def set_trainable(self, g: "ParamGroup", on: bool) -> None:
+        self.trainable[int(g)] = bool(on)
 
 
 def params_fingerprint(p: NetworkParams) -> str:

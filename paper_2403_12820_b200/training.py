@@ -224,12 +224,18 @@ class Trainer:
         rp = resume.params.to_c() if resume else None
         rtr = np.array([1 if t else 0 for t in resume.params.trainable], np.uint8) if resume \
             else None
+        br = np.zeros(14)
         _raise(self.lib, self.lib.sc_trainer_run(
             self.h, C.byref(c), C.byref(rp) if rp is not None else None, _ptr(rtr),
-            C.byref(opt), C.byref(out), _ptr(tr), _ptr(hist)))
+            C.byref(opt), C.byref(out), _ptr(tr), _ptr(hist), _ptr(br)))
         history = [LossRow(int(r[0]), float(r[1]), float(r[2]), float(r[3]), float(r[4]))
                    for r in hist[:cfg.epochs]]
-        return TrainResult(_params_from_c(out, tr), AdamState.from_c(opt), history)
+        params = _params_from_c(out, tr)
+        if resume is not None:  # fine-tune mode keeps the resumed parameters' brackets
+            params.brackets = list(resume.params.brackets)
+        else:
+            params.brackets = [(float(br[2 * g]), float(br[2 * g + 1])) for g in range(7)]
+        return TrainResult(params, AdamState.from_c(opt), history)
 
 
 def sample_indices(frames: int, batch_size: int, rng_seed: int) -> np.ndarray:

@@ -225,3 +225,147 @@ def evaluate(test: Trajectory, reference: Trajectory, device: int = 0) -> EvalRe
     rep.mean_error_pct = total / float(len(rep.frame_error_pct))
     rep.final_error_pct = rep.frame_error_pct[-1]
     return rep
+
+
+# ---- checkpoints (CKP1, io.cpp:495-606) and the loss CSV (io.cpp:596-604) ---------------------
+
+CKP_MAGIC = b"CKP1"
+GROUP_NAMES = ("kernel", "linear", "bias", "nonlinear", "deriv", "self_velocity", "alpha")
+GROUP_SIZES = (12, 12, 3, 12, 12, 1, 1)
+
+
+@dataclass
+class Checkpoint:
+    """Checkpoint (io.hpp:36-45; binding bindings.cpp:129-133): parameters with trainable flags
+    and init brackets, the optional Adam state, the step counter and a config echo."""
+    params: object = None
+    opt: object = None
+    step: int = 0
+    config_echo: str = ""
+
+
+def _group_slices():
+    out, k = [], 0
+    for n in GROUP_SIZES:
+        out.append(slice(k, k + n))
+        k += n
+    return out
+
+
+def save_checkpoint(path: str, checkpoint: Checkpoint) -> None:
+    """save_checkpoint (io.cpp:495-530), atomic write."""
+    from .scene import NetworkParams, channel_order_hash
+
+    p = checkpoint.params if checkpoint.params is not None else NetworkParams()
+    flat = p.scalars()
+    echo = checkpoint.config_echo.encode() if isinstance(checkpoint.config_echo, str) \
+        else bytes(checkpoint.config_echo)
+
+    def write(f):
+        f.write(CKP_MAGIC)
+        f.write(struct.pack("<IQqI", 1, channel_order_hash(), int(checkpoint.step), len(echo)))
+        f.write(echo)
+        f.write(struct.pack("<I", len(GROUP_NAMES)))
+        for g, (name, sl) in enumerate(zip(GROUP_NAMES, _group_slices())):
+            lo, hi = p.brackets[g]
+            vals = flat[sl]
+            f.write(struct.pack("<B", len(name)) + name.encode())
+            f.write(struct.pack("<BddI", 1 if p.trainable[g] else 0, float(lo), float(hi), len(vals)))
+            f.write(struct.pack("<%dd" % len(vals), *vals))
+        o = checkpoint.opt
+        f.write(struct.pack("<B", 1 if o is not None else 0))
+        if o is not None:
+            f.write(struct.pack("<q", int(o.step)))
+            f.write(np.ascontiguousarray(o.m, "<f8").tobytes())
+            f.write(np.ascontiguousarray(o.v, "<f8").tobytes())
+
+    _atomic_write(path, write)
+
+
+def load_checkpoint(path: str) -> Checkpoint:
+    """load_checkpoint (io.cpp:532-590): every validation and error text of the reference."""
+    from .scene import NetworkParams, channel_order_hash
+    from .training import AdamState
+
+    try:
+        with open(path, "rb") as f:
+            buf = f.read()
+    except OSError:
+        raise IoError("cannot open checkpoint %s" % path) from None
+    pos = [0]
+
+    def take(fmt, what):
+        n = struct.calcsize(fmt)
+        if len(buf) - pos[0] < n:
+            raise IoError("truncated file: expected %d more bytes of %s" % (n, what))
+        v = struct.unpack_from(fmt, buf, pos[0])
+        pos[0] += n
+        return v[0] if len(v) == 1 else v
+
+    def take_bytes(n, what):
+        if len(buf) - pos[0] < n:
+            raise IoError("truncated file: expected %d more bytes of %s" % (n, what))
+        b = buf[pos[0]:pos[0] + n]
+        pos[0] += n
+        return b
+
+    try:
+        if take_bytes(4, "checkpoint magic") != CKP_MAGIC:
+            raise IoError("not a checkpoint file (bad magic)")
+        version = take("<I", "checkpoint version")
+        if version != 1:
+            raise IoError("unsupported checkpoint version %d" % version)
+        if take("<Q", "channel order hash") != channel_order_hash():
+            raise IoError("checkpoint was written against a different stencil channel ordering")
+        ckp = Checkpoint(params=NetworkParams())
+        ckp.step = take("<q", "step counter")
+        echo_len = take("<I", "config echo length")
+        if echo_len > (1 << 20):
+            raise IoError("checkpoint config echo implausibly large")
+        ckp.config_echo = take_bytes(echo_len, "config echo").decode("utf-8", "surrogateescape")
+        groups = take("<I", "group count")
+        if groups != len(GROUP_NAMES):
+            raise IoError("checkpoint declares %d parameter groups, expected %d"
+                          % (groups, len(GROUP_NAMES)))
+        flat = [0.0] * 53
+        for g, (expected, sl) in enumerate(zip(GROUP_NAMES, _group_slices())):
+            name_len = take("<B", "group name length")
+            name = take_bytes(name_len, "group name").decode("utf-8", "surrogateescape")
+            if name != expected:
+                raise IoError('checkpoint group %d is "%s", expected "%s"' % (g, name, expected))
+            ckp.params.trainable[g] = take("<B", "trainable flag") != 0
+            lo = take("<d", "bracket")
+            hi = take("<d", "bracket")
+            ckp.params.brackets[g] = (lo, hi)
+            count = take("<I", "group scalar count")
+            if count != GROUP_SIZES[g]:
+                raise IoError('checkpoint group "%s" has %d scalars, expected %d'
+                              % (name, count, GROUP_SIZES[g]))
+            vals = take_bytes(8 * count, "group scalars")
+            flat[sl] = list(struct.unpack("<%dd" % count, vals))
+        trainable, brackets = ckp.params.trainable, ckp.params.brackets
+        ckp.params = NetworkParams.from_scalars(flat)
+        ckp.params.trainable, ckp.params.brackets = trainable, brackets
+        if not (ckp.params.isru_alpha > 0.0):
+            raise IoError("checkpoint isru_alpha must be > 0")
+        if take("<B", "optimizer flag") != 0:
+            step = take("<q", "optimizer step")
+            m = np.frombuffer(take_bytes(8 * 53, "optimizer moments"), "<f8").copy()
+            v = np.frombuffer(take_bytes(8 * 53, "optimizer moments"), "<f8").copy()
+            ckp.opt = AdamState(m, v, step)
+        return ckp
+    except IoError as e:
+        raise IoError("%s: %s" % (path, e)) from None
+
+
+def write_loss_csv(path: str, rows) -> None:
+    """write_loss_csv (io.cpp:596-604): rows of LossRow or (step, lr, physics, data, total)."""
+    def write(f):
+        lines = ["step,lr,physics,data,total"]
+        for r in rows:
+            t = (r.step, r.lr, r.physics, r.data, r.total) if hasattr(r, "step") else tuple(r)
+            lines.append("%d,%s,%s,%s,%s" % (int(t[0]), _g17(t[1]), _g17(t[2]), _g17(t[3]),
+                                             _g17(t[4])))
+        f.write(("\n".join(lines) + "\n").encode())
+
+    _atomic_write(path, write)

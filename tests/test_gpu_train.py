@@ -182,3 +182,41 @@ def test_gradient_check_matches_reference_module():
     for args in ((8, 8, 7, 1e-6), (5, 9, 3, 1e-5)):
         assert ours.gradient_check(*args) == sc.gradient_check(*args)
     assert ours.gradient_check() < 1e-5
+
+
+def test_train_binding_checkpoint_bytes_match_reference(tmp_path):
+    """The reference module's own train() and ours on the same parsed scene and simulated
+    trajectory: the CKP1 files of the two results are byte-identical (parameters, trainable
+    flags and the DE brackets)."""
+    import os
+    import sys
+    ref_pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                           "_ref")
+    if not os.path.isdir(os.path.join(ref_pkg, "stencilcloth")):
+        pytest.skip("reference module not built")
+    sys.path.insert(0, ref_pkg)
+    import stencilcloth as sc
+    text = """{"name": "ckp_train", "grid": {"nx": 10, "ny": 8, "spacing": 0.05,
+      "origin": [-0.2, -0.15, 0.3], "plane": "xy"},
+      "material": {"stiffness": 30.0, "damping": 0.05, "mass": 0.01,
+                   "gravity": [0.0, 0.0, -9.8], "drag": 0.02, "pressure": 0.2},
+      "time": {"dt": 0.001, "steps": 40}, "pins": {"nodes": ["top_left", "top_right"]},
+      "colliders": [{"type": "sphere", "center": [0.0, 0.0, 0.0], "radius": 0.25,
+                     "friction": 0.3}]}"""
+    rscene = sc.parse_scene(text)
+    rtraj = sc.simulate(rscene)
+    kw = dict(alpha=0.4, batch_size=6, epochs=8, seed=5, lr0=2e-2, de_population=5,
+              de_generations=2, de_probe=4)
+    rparams, rhist = sc.train(rscene, rtraj, **kw)
+    scene = ours.parse_scene(text)
+    traj = ours.simulate(scene)
+    assert bits(traj.frames_x, np.stack([rtraj.positions(f) for f in range(rtraj.frame_count)]))
+    params, hist = ours.train(scene, traj, **kw)
+    assert bits(np.array(hist), np.array(rhist))
+    pr, po = str(tmp_path / "ref.ckpt"), str(tmp_path / "ours.ckpt")
+    rc = sc.Checkpoint()
+    rc.params = rparams
+    rc.step = kw["epochs"]
+    sc.save_checkpoint(pr, rc)
+    ours.save_checkpoint(po, ours.Checkpoint(params, None, kw["epochs"], ""))
+    assert open(po, "rb").read() == open(pr, "rb").read()
