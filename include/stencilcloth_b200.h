@@ -187,6 +187,10 @@ sc_status sc_nn_step(sc_ctx* ctx, const void* x, const void* v, double t_next, s
  * naming the first node ("elastic force: singular spring ...", kernels.hpp:105-107). */
 sc_status sc_total_impulse(sc_ctx* ctx, const void* x, const void* v, void* impulse);
 /* step_semi_implicit (sim.hpp:58 / sim.cpp:150-155) from host state to host state. */
+/* total_force (sim.cpp:84-96; binding total_force, bindings.cpp:156-161): the four force terms
+ * accumulated in the reference order, unscaled, [batch][node][3]. Same errors as
+ * sc_total_impulse. */
+sc_status sc_total_force(sc_ctx* ctx, const void* x, const void* v, void* force);
 sc_status sc_pbs_step(sc_ctx* ctx, const void* x, const void* v, double t_next, void* x_out,
                       void* v_out, uint8_t* constrained);
 /* simulate_scene's stepping (sim.cpp:157-175) with frame storage like sc_rollout_frames; after

@@ -17,7 +17,7 @@ from .scene import (BoundarySpec, ConfigError, GridPlane, IoError, MaterialParam
 from .api import (BenchResult, ClothBatch, Context, CudaError, advance_with_impulse,  # noqa: E402
                   apply_dirichlet, benchmark_net, benchmark_sim, forward_impulse, nn_step,
                   pinned_empty, plug_impulse, rollout, simulate, step_semi_implicit,
-                  total_impulse)
+                  total_force, total_impulse)
 from .training import (AdamState, DeConfig, LossRow, LossValue, ParamGradients,  # noqa: E402
                     ScheduleConfig, ScheduleKind, TrainConfig, Trainer, TrainResult,
                     backward_gradients, gradient_check, sample_indices, train,
@@ -32,7 +32,7 @@ __all__ = [
     "PlaneCollider", "PlugForce", "Scene", "SphereCollider", "Trajectory", "advance_with_impulse",
     "apply_dirichlet", "benchmark_net", "build_grid", "channel_order_hash", "forward_impulse",
     "load_scene", "nn_step", "params_fingerprint", "parse_scene", "plug_impulse", "rollout",
-    "benchmark_sim", "simulate", "step_semi_implicit", "total_impulse",
+    "benchmark_sim", "simulate", "step_semi_implicit", "total_force", "total_impulse",
     "EvalReport", "evaluate", "export_obj", "load_trajectory", "pinned_empty", "save_trajectory",
     "write_eval_csv", "Checkpoint", "load_checkpoint", "save_checkpoint", "write_loss_csv",
     "AdamState", "DeConfig", "LossRow", "LossValue", "ParamGradients",

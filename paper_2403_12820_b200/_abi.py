@@ -127,6 +127,7 @@ SIGNATURES = {
     "sc_pbs_step": (C.c_int, [_P, _P, _P, C.c_double, _P, _P, _P]),
     "sc_simulate_frames": (C.c_int, [_P, _P, _P, _I, _I, _P, _P]),
     "sc_benchmark_sim": (C.c_int, [_P, _I, _I, C.POINTER(C.c_double)]),
+    "sc_total_force": (C.c_int, [_P, _P, _P, _P]),
     "sc_evaluate_frames": (C.c_int, [C.c_int, _P, _P, _I, C.c_int64, _P]),
     "sc_eval_last_error": (C.c_char_p, []),
     "sc_trainer_create": (C.c_int, [C.c_int, _P, _I, _P, _P, C.POINTER(_P)]),

@@ -213,6 +213,12 @@ class Context:
         _raise(self.lib, self.lib.sc_total_impulse(self.h, _ptr(x), _ptr(v), _ptr(out)))
         return out
 
+    def total_force(self, x, v) -> np.ndarray:
+        x, v = self._arr(x), self._arr(v)
+        out = self._empty()
+        _raise(self.lib, self.lib.sc_total_force(self.h, _ptr(x), _ptr(v), _ptr(out)))
+        return out
+
     def pbs_step(self, x, v, t_next: float, constrained: bool = False):
         x, v = self._arr(x), self._arr(v)
         xo, vo = self._empty(), self._empty()
@@ -496,6 +502,15 @@ def total_impulse(scene: Scene, positions, velocities, device: int = 0) -> np.nd
     _check_shape(x, v, scene)
     with Context(scene, None, "f64", device) as ctx:
         return ctx.total_impulse(x, v)[0]
+
+
+def total_force(scene: Scene, positions, velocities, device: int = 0) -> np.ndarray:
+    """Sum of the elastic, damping, pressure and external forces (sim.cpp:84-96; binding
+    total_force, bindings.cpp:156-161), float64, bit-identical to the reference."""
+    x, v = _state2(positions, 0, "positions"), _state2(velocities, 0, "velocities")
+    _check_shape(x, v, scene)
+    with Context(scene, None, "f64", device) as ctx:
+        return ctx.total_force(x, v)[0]
 
 
 def step_semi_implicit(scene: Scene, positions, velocities, t_next: float, device: int = 0):

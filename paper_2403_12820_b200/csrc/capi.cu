@@ -945,13 +945,13 @@ sc_status op_entry(sc_ctx* c, int kind, sc_mode mode, const void* x, const void*
     if (mode == SC_MODE_FAST && c->prec != SC_F32) throw_config("mode: FAST is an f32 mode");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_health(c);
-    if ((kind == KIND_PBS || kind == KIND_TOTAL) && !c->pbs_ok)
+    if ((kind == KIND_PBS || kind == KIND_TOTAL || kind == KIND_FORCE) && !c->pbs_ok)
       throw_config("grid.spacing: must be a finite value > 0 (rest lengths of the PBS step)");
     if (c->prec == SC_F32)
       op_call<float>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
     else
       op_call<double>(c, kind, mode, x, v, imp_in, imp_out, t_next, xo, vo, constrained);
-    if (kind == KIND_PBS || kind == KIND_TOTAL) pbs_check(c, kind == KIND_PBS);
+    if (kind == KIND_PBS || kind == KIND_TOTAL || kind == KIND_FORCE) pbs_check(c, kind == KIND_PBS);
   });
 }
 }  // namespace
@@ -1001,6 +1001,15 @@ sc_status sc_total_impulse(sc_ctx* c, const void* x, const void* v, void* impuls
     return SC_ERR_CONFIG;
   }
   return op_entry(c, KIND_TOTAL, SC_MODE_PARITY, x, v, nullptr, impulse, 0.0, nullptr, nullptr,
+                  nullptr, false);
+}
+
+sc_status sc_total_force(sc_ctx* c, const void* x, const void* v, void* force) {
+  if (!force) {
+    g_err = "force: null array";
+    return SC_ERR_CONFIG;
+  }
+  return op_entry(c, KIND_FORCE, SC_MODE_PARITY, x, v, nullptr, force, 0.0, nullptr, nullptr,
                   nullptr, false);
 }
 

@@ -9,6 +9,7 @@
 //   KIND_PBS     total_impulse -> advance_with_impulse: step_semi_implicit (sim.cpp:150-155),
 //                the ground-truth mass-spring step
 //   KIND_TOTAL   total_impulse only (kernels.hpp:165-175)
+//   KIND_FORCE   total_force: the same four accumulations, unscaled (sim.cpp:84-96)
 // Every floating-point operation is a non-contractible IEEE RN primitive in the reference's
 // order; this TU is additionally compiled with --fmad=false.
 //
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
             (static_cast<unsigned long long>(a.k + 1) << 32) | static_cast<unsigned long long>(gnode);
         atomicMin(&a.health[b].impulse_key, key);
       }
-    } else if (KIND == KIND_PBS || KIND == KIND_TOTAL) {
+    } else if (KIND == KIND_PBS || KIND == KIND_TOTAL || KIND == KIND_FORCE) {
       // total_impulse<T> (kernels.hpp:165-175): elastic, damping, pressure, external, * dt/m
       T f[3] = {T(0), T(0), T(0)};
       bool singular = false;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) {  // accumulate_external (kernels.hpp:159-162), then * dt/m
         f[d] = R::add(f[d], R::sub(R::mul(cc.grav[d], cc.mass), R::mul(v[d], cc.drag)));
-        imp[d] = R::mul(f[d], cc.scale);
+        imp[d] = KIND == KIND_FORCE ? f[d] : R::mul(f[d], cc.scale);
       }
       if (singular && a.health) {
         const unsigned long long key =
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
       plug_tail(cc, v, imp);
     }
 
-    if (KIND == KIND_FORWARD || KIND == KIND_PLUG || KIND == KIND_TOTAL) {
+    if (KIND == KIND_FORWARD || KIND == KIND_PLUG || KIND == KIND_TOTAL || KIND == KIND_FORCE) {
       T* op = a.impulse + (static_cast<int64_t>(b) * nodes + gnode) * 3;
 #pragma unroll
       for (int d = 0; d < 3; ++d) op[d] = imp[d];
@@ -254,6 +255,8 @@ cudaError_t launch_parity(const StepArgs<T>& a, int kind, cudaStream_t stream) {
       return launch_parity_t<T, KIND_PBS>(a, stream);
     case KIND_TOTAL:
       return launch_parity_t<T, KIND_TOTAL>(a, stream);
+    case KIND_FORCE:
+      return launch_parity_t<T, KIND_FORCE>(a, stream);
   }
   return cudaErrorInvalidValue;
 }

@@ -10,7 +10,15 @@
 
 namespace scb {
 
-enum { KIND_STEP = 0, KIND_FORWARD = 1, KIND_PLUG = 2, KIND_ADVANCE = 3, KIND_PBS = 4, KIND_TOTAL = 5 };
+enum {
+  KIND_STEP = 0,
+  KIND_FORWARD = 1,
+  KIND_PLUG = 2,
+  KIND_ADVANCE = 3,
+  KIND_PBS = 4,
+  KIND_TOTAL = 5,
+  KIND_FORCE = 6
+};
 
 // parity_kernels.cu (compiled with --fmad=false)
 template <typename T>

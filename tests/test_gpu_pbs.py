@@ -77,3 +77,34 @@ def test_pbs_errors_match_reference(reference):
     with pytest.raises(ArithmeticError) as e_gpu:
         sc.simulate(scene)
     assert str(e_gpu.value) == str(e_ref.value)
+
+
+def test_total_force_matches_reference_module():
+    """total_force (sim.cpp:84-96) through the reference's own binding, bit for bit, including
+    its singular-spring error text."""
+    import os
+    import sys
+    ref_pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                           "_ref")
+    if not os.path.isdir(os.path.join(ref_pkg, "stencilcloth")):
+        pytest.skip("reference module not built")
+    sys.path.insert(0, ref_pkg)
+    import stencilcloth as ref
+    import paper_2403_12820_b200 as sc
+    text = """{"name": "tf", "grid": {"nx": 11, "ny": 9, "spacing": 0.05,
+      "origin": [-0.25, -0.2, 0.3], "plane": "xy"},
+      "material": {"stiffness": 40.0, "damping": 0.3, "mass": 0.02,
+                   "gravity": [0.1, 0.0, -9.8], "drag": 0.05, "pressure": 0.7},
+      "time": {"dt": 0.001, "steps": 10}, "pins": {"nodes": ["top_left"]}}"""
+    rscene = ref.parse_scene(text)
+    scene = sc.parse_scene(text)
+    rng = np.random.default_rng(4)
+    x = rscene.initial_positions() + rng.normal(0, 0.01, (99, 3))
+    v = rng.normal(0, 0.5, (99, 3))
+    assert bits_equal(sc.total_force(scene, x, v), ref.total_force(rscene, x, v))
+    x[5] = x[6]  # coincident connected pair
+    with pytest.raises(ArithmeticError) as r:
+        ref.total_force(rscene, x, v)
+    with pytest.raises(sc.NumericsError) as o:
+        sc.total_force(scene, x, v)
+    assert str(o.value) == str(r.value)
