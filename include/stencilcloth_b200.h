@@ -305,6 +305,26 @@ void* sc_ctx_stream(sc_ctx* ctx);
 sc_status sc_ctx_state_buffers(sc_ctx* ctx, void** front, void** back, int64_t* plane_stride,
                                int32_t* pitch, int32_t* local_rows, int32_t* row_base);
 
+/* ---- fused halo exchange over peer memory (§8(e), config 4 strips) ------------------------ */
+/* A strip context exports its two state buffers and its completion flags (CUDA IPC handles and
+ * raw pointers); a neighbour links them with sc_ctx_set_peer (side 0: the strip below, 1: above;
+ * use_ipc = 0 for contexts in the same process). sc_ctx_peer_step then runs one FAST step of
+ * the whole owned strip in which the two boundary rows at each linked side are also stored
+ * straight into the neighbour's ghost rows (NVLink peer stores), bracketed by a wait on the
+ * neighbours' completion flags and a system-scope release of ours: no NCCL call, no pack. */
+typedef struct sc_peer_export {
+  unsigned char state_handle[2][64]; /* cudaIpcMemHandle_t of state buffers 0 and 1 */
+  unsigned char flags_handle[64];
+  void* state_ptr[2]; /* raw device pointers (same-process linking) */
+  void* flags_ptr;
+  int64_t plane_stride;
+  int32_t g0, u0, u1, nx, pitch, batch, cur, device;
+} sc_peer_export;
+sc_status sc_ctx_peer_export(sc_ctx* ctx, sc_peer_export* out);
+sc_status sc_ctx_set_peer(sc_ctx* ctx, int32_t side, const sc_peer_export* neighbour,
+                          int32_t use_ipc);
+sc_status sc_ctx_peer_step(sc_ctx* ctx, int32_t k, sc_mode mode, void* stream);
+
 /* Page-locked host buffers, so host<->device copies of rollout() run at full PCIe/C2C rate. */
 sc_status sc_host_alloc(size_t bytes, void** out);
 void sc_host_free(void* p);

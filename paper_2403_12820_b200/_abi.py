@@ -58,6 +58,19 @@ class sc_adam_state(C.Structure):
     _fields_ = [("m", C.c_double * 53), ("v", C.c_double * 53), ("step", C.c_int64)]
 
 
+class sc_peer_export(C.Structure):
+    """sc_peer_export: a strip context's IPC handles / pointers for a neighbour to link."""
+    _fields_ = [
+        ("state_handle", (C.c_ubyte * 64) * 2),
+        ("flags_handle", C.c_ubyte * 64),
+        ("state_ptr", C.c_void_p * 2),
+        ("flags_ptr", C.c_void_p),
+        ("plane_stride", C.c_int64),
+        ("g0", C.c_int32), ("u0", C.c_int32), ("u1", C.c_int32), ("nx", C.c_int32),
+        ("pitch", C.c_int32), ("batch", C.c_int32), ("cur", C.c_int32), ("device", C.c_int32),
+    ]
+
+
 class sc_sphere(C.Structure):
     _fields_ = [("center", C.c_double * 3), ("radius", C.c_double), ("friction", C.c_double)]
 
@@ -146,6 +159,9 @@ SIGNATURES = {
     "sc_ctx_halo_unpack": (C.c_int, [_P, _I, _P, _P]),
     "sc_ctx_strip_step": (C.c_int, [_P, _I, _I, _I, C.c_int, _P]),
     "sc_ctx_strip_commit": (C.c_int, [_P]),
+    "sc_ctx_peer_export": (C.c_int, [_P, C.POINTER(sc_peer_export)]),
+    "sc_ctx_set_peer": (C.c_int, [_P, _I, C.POINTER(sc_peer_export), _I]),
+    "sc_ctx_peer_step": (C.c_int, [_P, _I, C.c_int, _P]),
     "sc_ctx_stream": (_P, [_P]),
     "sc_ctx_state_buffers": (
         C.c_int,

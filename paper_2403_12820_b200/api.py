@@ -274,6 +274,22 @@ class Context:
                                                     MODES[mode],
                                                     C.c_void_p(stream) if stream else None))
 
+    def peer_export(self) -> bytes:
+        """This strip context's IPC handles / pointers (sc_ctx_peer_export) as bytes."""
+        e = _abi.sc_peer_export()
+        _raise(self.lib, self.lib.sc_ctx_peer_export(self.h, C.byref(e)))
+        return bytes(e)
+
+    def set_peer(self, side: int, export: bytes, ipc: bool = True) -> None:
+        """Link the neighbour strip on `side` (0: below, 1: above) from its peer_export()."""
+        e = _abi.sc_peer_export.from_buffer_copy(export)
+        _raise(self.lib, self.lib.sc_ctx_set_peer(self.h, int(side), C.byref(e), 1 if ipc else 0))
+
+    def peer_step(self, k: int, mode: str = "fast", stream: Optional[int] = None) -> None:
+        """One fused step: boundary rows stored straight into the linked neighbours' ghost rows."""
+        _raise(self.lib, self.lib.sc_ctx_peer_step(self.h, int(k), MODES[mode],
+                                                   C.c_void_p(stream) if stream else None))
+
     def strip_commit(self) -> None:
         _raise(self.lib, self.lib.sc_ctx_strip_commit(self.h))
 

@@ -137,6 +137,20 @@ struct sc_ctx {
   bool tmap_ok = false;
   std::atomic<int64_t> launches{0};
   bool health_on = false;  // non-finite tracking in device-resident stepping
+  // fused halo exchange with strip neighbours (sc_ctx_set_peer / sc_ctx_peer_step): side 0 =
+  // the neighbour owning the rows below, 1 = above
+  struct Peer {
+    void* buf[2] = {nullptr, nullptr};  // its state buffers (IPC-mapped or same-process)
+    int64_t S = 0;
+    int32_t g0 = 0;
+    int32_t cur_delta = 0;              // its buffer parity relative to ours
+    unsigned* flag = nullptr;           // its completion-flag slot this ctx signals
+    bool ipc = false;
+    void* opened[3] = {nullptr, nullptr, nullptr};
+  } peer[2];
+  DevBuf<unsigned> peer_flags;  // [2] written by the neighbours: steps they have completed
+  unsigned peer_count = 0;      // fused steps this ctx has completed since linking
+  bool peer_launch = false;     // base_args adds the peer stores
   // frame streaming (sc_rollout_frames / sc_simulate_frames): two pinned host slots + events
   void* pin_stage = nullptr;
   size_t pin_stage_bytes = 0;
@@ -427,6 +441,14 @@ StepArgs<T> base_args(sc_ctx* c) {
   a.pin_bits = c->pin_bits.p;
   a.pin_rank = c->pin_rank.p;
   a.pin_anchors = static_cast<const T*>(c->anchors);
+  if (c->peer_launch)
+    for (int sd = 0; sd < 2; ++sd) {
+      const sc_ctx::Peer& q = c->peer[sd];
+      if (!q.buf[0]) continue;
+      a.peer_out[sd] = static_cast<T*>(q.buf[1 - (c->cur ^ q.cur_delta)]);
+      a.peer_S[sd] = q.S;
+      a.peer_g0[sd] = q.g0;
+    }
   return a;
 }
 
@@ -695,6 +717,10 @@ void sc_ctx_destroy(sc_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (cudaEvent_t e : c->frame_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& q : c->peer)
+    for (void* o : q.opened)
+      if (o) cudaIpcCloseMemHandle(o);
+  c->peer_flags.release();
   if (c->pin_stage) cudaFreeHost(c->pin_stage);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1196,6 +1222,145 @@ sc_status sc_ctx_state_buffers(sc_ctx* c, void** front, void** back, int64_t* pl
     if (pitch) *pitch = c->pitch;
     if (local_rows) *local_rows = c->rows_local;
     if (row_base) *row_base = c->g0;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// Peer-step handshake. A neighbour writes `steps completed` into our flag slot after each fused
+// step (system-scope release after a system fence, so its remote ghost-row stores are visible
+// first); before our n-th step we wait for n from both neighbours: their step n-1 wrote our
+// ghost rows, and they are done reading the buffer whose ghost rows our step n overwrites.
+__global__ void peer_wait_kernel(const unsigned* flags, int need0, int need1, unsigned target) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = clock64();
+  for (int sd = 0; sd < 2; ++sd) {
+    if (!(sd == 0 ? need0 : need1)) continue;
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + sd) : "memory");
+      if (v >= target) break;
+      __nanosleep(256);
+      if (clock64() - t0 > (1LL << 35)) __trap();  // ~15 s: a neighbour is gone
+    }
+  }
+}
+
+__global__ void peer_signal_kernel(unsigned* f0, unsigned* f1, unsigned val) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  if (f0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f0), "r"(val) : "memory");
+  if (f1) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f1), "r"(val) : "memory");
+}
+}  // namespace
+
+extern "C" {
+
+sc_status sc_ctx_peer_export(sc_ctx* c, sc_peer_export* out) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (!out) throw_config("peer export: null");
+    if (c->strip_row0 < 0) throw_config("peer export: context has no strip");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->peer_flags.ensure(2);
+    std::memset(out, 0, sizeof *out);
+    for (int i = 0; i < 2; ++i) {
+      cudaIpcMemHandle_t h;
+      ck(cudaIpcGetMemHandle(&h, c->state[i]), "cudaIpcGetMemHandle");
+      std::memcpy(out->state_handle[i], &h, sizeof h);
+      out->state_ptr[i] = c->state[i];
+    }
+    cudaIpcMemHandle_t hf;
+    ck(cudaIpcGetMemHandle(&hf, c->peer_flags.p), "cudaIpcGetMemHandle");
+    std::memcpy(out->flags_handle, &hf, sizeof hf);
+    out->flags_ptr = c->peer_flags.p;
+    out->plane_stride = c->plane_stride;
+    out->g0 = c->g0;
+    out->u0 = c->u0;
+    out->u1 = c->u1;
+    out->nx = c->nx;
+    out->pitch = c->pitch;
+    out->batch = c->batch;
+    out->cur = c->cur;
+    out->device = c->device;
+  });
+}
+
+sc_status sc_ctx_set_peer(sc_ctx* c, int32_t side, const sc_peer_export* nb, int32_t use_ipc) {
+  return guarded([&] {
+    require_ready(c, false);
+    if (c->strip_row0 < 0) throw_config("peer: context has no strip");
+    if (side != 0 && side != 1) throw_config("peer: side must be 0 or 1");
+    if (!nb) throw_config("peer: null export");
+    if (nb->nx != c->nx || nb->pitch != c->pitch || nb->batch != c->batch)
+      throw_config("peer: neighbour has a different grid layout");
+    if (side == 0 ? nb->u1 != c->u0 : nb->u0 != c->u1)
+      throw_config("peer: neighbour strip is not adjacent on that side");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    sc_ctx::Peer& q = c->peer[side];
+    for (void*& o : q.opened)
+      if (o) {
+        cudaIpcCloseMemHandle(o);
+        o = nullptr;
+      }
+    void* p[3];
+    if (use_ipc) {
+      for (int i = 0; i < 2; ++i) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, nb->state_handle[i], sizeof h);
+        ck(cudaIpcOpenMemHandle(&p[i], h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        q.opened[i] = p[i];
+      }
+      cudaIpcMemHandle_t hf;
+      std::memcpy(&hf, nb->flags_handle, sizeof hf);
+      ck(cudaIpcOpenMemHandle(&p[2], hf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      q.opened[2] = p[2];
+    } else {
+      p[0] = nb->state_ptr[0];
+      p[1] = nb->state_ptr[1];
+      p[2] = nb->flags_ptr;
+    }
+    q.buf[0] = p[0];
+    q.buf[1] = p[1];
+    q.S = nb->plane_stride;
+    q.g0 = nb->g0;
+    q.cur_delta = (nb->cur ^ c->cur) & 1;
+    q.ipc = use_ipc != 0;
+    // we are its neighbour on the opposite side
+    q.flag = static_cast<unsigned*>(p[2]) + (side == 0 ? 1 : 0);
+    c->peer_flags.ensure(2);
+    ck(cudaMemset(c->peer_flags.p, 0, 2 * sizeof(unsigned)), "memset");
+    c->peer_count = 0;
+  });
+}
+
+sc_status sc_ctx_peer_step(sc_ctx* c, int32_t k, sc_mode mode, void* stream) {
+  return guarded([&] {
+    require_ready(c);
+    if (c->strip_row0 < 0) throw_config("peer step: context has no strip");
+    if (mode != SC_MODE_FAST || c->prec != SC_F32)
+      throw_config("peer step: the fused exchange runs in FAST f32 mode");
+    if (!c->peer[0].buf[0] && !c->peer[1].buf[0]) throw_config("peer step: no peer linked");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    peer_wait_kernel<<<1, 32, 0, st>>>(c->peer_flags.p, c->peer[0].buf[0] != nullptr,
+                                       c->peer[1].buf[0] != nullptr, c->peer_count);
+    ck(cudaGetLastError(), "peer wait");
+    c->peer_launch = true;
+    Health* h = c->health_on ? c->health.p : nullptr;
+    try {
+      launch_one<float>(c, KIND_STEP, mode, k, false, 0.0, nullptr, nullptr, h, c->u0, c->u1, st);
+    } catch (...) {
+      c->peer_launch = false;
+      throw;
+    }
+    c->peer_launch = false;
+    peer_signal_kernel<<<1, 32, 0, st>>>(c->peer[0].flag, c->peer[1].flag, c->peer_count + 1);
+    ck(cudaGetLastError(), "peer signal");
+    c->launches.fetch_add(2);
+    c->peer_count += 1;
+    c->cur = 1 - c->cur;
   });
 }
 

@@ -468,7 +468,7 @@ __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int 
 // One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
 // tensor maps and writing a.out. `phase` carries the ring barriers' parity bits across calls
 // (the persistent kernel runs many units / steps on the same ring).
-template <bool ALPHA1, int RING>
+template <bool ALPHA1, int RING, bool PEER = false>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
                                          const StepArgs<float>& a, const FastNet& f, int b,
                                          int strip, int y0, int y1, float* ring, uint64_t* full,
@@ -645,6 +645,28 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         reinterpret_cast<float4*>(ovxy)[1] = make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
         *reinterpret_cast<float4*>(oz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
         *reinterpret_cast<float4*>(oz + S) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
+        // fused halo exchange: the two owned rows at a peer side also go into the neighbour's
+        // ghost rows (its output buffer, remote over NVLink)
+        if (PEER && (Rf < a.u0 + 2 || Rf >= a.u1 - 2))  // boundary rows only
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          float* po = a.peer_out[side];
+          if (po == nullptr) continue;
+          if (side == 0 ? Rf >= a.u0 + 2 : Rf < a.u1 - 2) continue;
+          const int64_t S2 = a.peer_S[side];
+          const int64_t lr2 = Rf - a.peer_g0[side];
+          float* pb = po + static_cast<int64_t>(b) * 6 * S2;
+          float* pxy = pb + 2 * (lr2 * a.pitch + ix0);
+          float* pz = pb + 4 * S2 + lr2 * a.pitch + ix0;
+          reinterpret_cast<float4*>(pxy)[0] = make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
+          reinterpret_cast<float4*>(pxy)[1] = make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
+          reinterpret_cast<float4*>(pxy + 2 * S2)[0] =
+              make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
+          reinterpret_cast<float4*>(pxy + 2 * S2)[1] =
+              make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
+          *reinterpret_cast<float4*>(pz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
+          *reinterpret_cast<float4*>(pz + S2) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
+        }
       } else {
         // colliders / pressure / mask: one node at a time (compact code, same IEEE-exact chain)
         const float* rs = ring + s3 * ROWF;  // row Rf-1
@@ -690,6 +712,18 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           for (int d = 0; d < 3; ++d) {
             out_b[elem_index(d, lr, ix, a.pitch, S)] = po[d];
             out_b[elem_index(3 + d, lr, ix, a.pitch, S)] = qo[d];
+          }
+          for (int side = 0; PEER && side < 2; ++side) {  // fused halo exchange (simple path)
+            float* pp = a.peer_out[side];
+            if (pp == nullptr || (side == 0 ? Rf >= a.u0 + 2 : Rf < a.u1 - 2)) continue;
+            const int64_t S2 = a.peer_S[side];
+            float* pb = pp + static_cast<int64_t>(b) * 6 * S2;
+            const int64_t lr2 = Rf - a.peer_g0[side];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              pb[elem_index(d, lr2, ix, a.pitch, S2)] = po[d];
+              pb[elem_index(3 + d, lr2, ix, a.pitch, S2)] = qo[d];
+            }
           }
           if (a.constrained) a.constrained[b * nodes + gnode] = mk;
           if (a.health && !(isfinite(po[0]) && isfinite(po[1]) && isfinite(po[2]) &&
@@ -741,7 +775,7 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 #ifndef SC_FAST_MINB
 #define SC_FAST_MINB 16
 #endif
-template <bool ALPHA1, int RING>
+template <bool ALPHA1, int RING, bool PEER = false>
 __global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
@@ -774,7 +808,8 @@ __global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __gri
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch, phase);
+    run_unit<ALPHA1, RING, PEER>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
+                                 phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
   // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
@@ -896,6 +931,11 @@ void* pick_kernel(bool alpha1, int ring) {
 }
 
 template <bool ALPHA1, int RING>
+void* peer_kernel_ptr() {
+  return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, true>);
+}
+
+template <bool ALPHA1, int RING>
 void* multi_ptr() {
   return reinterpret_cast<void*>(fast_multi_kernel<ALPHA1, RING>);
 }
@@ -920,7 +960,9 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = fast_smem_bytes(p.ring, general);
   for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring), pick_multi(true, p.ring),
-                  pick_multi(false, p.ring)})
+                  pick_multi(false, p.ring),
+                  p.ring == 5 ? peer_kernel_ptr<true, 5>() : peer_kernel_ptr<true, 4>(),
+                  p.ring == 5 ? peer_kernel_ptr<false, 5>() : peer_kernel_ptr<false, 4>()})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
@@ -988,12 +1030,15 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   const CUtensorMap& txy = tmap[0];
   const CUtensorMap& tz = tmap[1];
   const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
-  if (p.ring == 5) {
-    if (f.alpha1) return cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 5>, txy, tz, a, f, ns, sr, ng);
-    return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 5>, txy, tz, a, f, ns, sr, ng);
+  const bool peer = a.peer_out[0] != nullptr || a.peer_out[1] != nullptr;
+#define SC_FK(A, R, P) cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P>, txy, tz, a, f, ns, sr, ng)
+  if (peer) {  // fused halo exchange (strip contexts linked with sc_ctx_set_peer)
+    if (p.ring == 5) return f.alpha1 ? SC_FK(true, 5, true) : SC_FK(false, 5, true);
+    return f.alpha1 ? SC_FK(true, 4, true) : SC_FK(false, 4, true);
   }
-  if (f.alpha1) return cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 4>, txy, tz, a, f, ns, sr, ng);
-  return cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4>, txy, tz, a, f, ns, sr, ng);
+  if (p.ring == 5) return f.alpha1 ? SC_FK(true, 5, false) : SC_FK(false, 5, false);
+  return f.alpha1 ? SC_FK(true, 4, false) : SC_FK(false, 4, false);
+#undef SC_FK
 }
 
 cudaError_t set_unit_timing(unsigned long long* dev_buf) {

@@ -145,6 +145,12 @@ struct StepArgs {
   uint8_t* constrained;     // [batch][ny*nx] global node index, or nullptr
   T* impulse;               // planar [batch][3][local plane] or nullptr (forward-only output)
   Health* health;           // [batch] or nullptr
+  // fused halo exchange (FAST strips with peer neighbours): the two owned rows next to side s
+  // are also stored into that neighbour's output buffer (peer_out[s], its plane stride and row
+  // base), i.e. straight into its ghost rows over NVLink. nullptr: no peer on that side.
+  T* peer_out[2];
+  int64_t peer_S[2];
+  int32_t peer_g0[2];
   NetConst<T> net;
 };
 

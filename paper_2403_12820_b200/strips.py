@@ -10,6 +10,11 @@ Per step:
   4. the received rows land in the ghost rows and the state buffers swap.
 Nodes, pins and masks keep their GLOBAL indices; only the state buffer is local, so every row
 is computed with exactly the arithmetic of the single-GPU kernel (bit-identical results).
+
+transport="peer" (FAST mode) replaces steps 1-4 by one fused kernel per step: the boundary rows
+are stored straight into the neighbours' ghost rows through CUDA IPC mappings of their state
+buffers (NVLink peer stores), with a completion-flag handshake instead of NCCL
+(sc_ctx_peer_step, csrc/capi.cu). The handles are exchanged once with all_gather_object.
 """
 from __future__ import annotations
 
@@ -67,12 +72,17 @@ class StripRollout:
     the cloth's global descriptor (global pins; positions not needed)."""
 
     def __init__(self, scene, params, x_local, v_local, rank: int, world: int, device: int = 0,
-                 group=None, mode: str = "fast"):
+                 group=None, mode: str = "fast", transport: str = "nccl"):
         import torch
 
         from .api import ClothBatch
 
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport: 'nccl' or 'peer'")
+        if transport == "peer" and mode != "fast":
+            raise ValueError("transport 'peer' runs the FAST kernel")
         self.rank, self.world, self.group, self.mode = rank, world, group, mode
+        self.transport = transport
         self.ny = scene.ny
         self.row0, self.rows = strip_bounds(scene.ny, world, rank)
         self.g0, self.g1 = local_window(scene.ny, self.row0, self.rows)
@@ -84,6 +94,21 @@ class StripRollout:
             torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(4))
         # a real (non-legacy) stream: kernels, packs and NCCL all order on it
         self.stream = torch.cuda.Stream(device=dev)
+        if transport == "peer" and world > 1:
+            import torch.distributed as dist
+            exports = [None] * world
+            dist.all_gather_object(exports, self.ctx.peer_export(), group=group)
+            if rank > 0:
+                self.ctx.set_peer(0, exports[rank - 1], ipc=True)
+            if rank < world - 1:
+                self.ctx.set_peer(1, exports[rank + 1], ipc=True)
+            dist.barrier(group=group)
+
+    @staticmethod
+    def link_local(lower: "StripRollout", upper: "StripRollout") -> None:
+        """Link two strips held by one process (same device) for the fused peer path."""
+        lower.ctx.set_peer(1, upper.ctx.peer_export(), ipc=False)
+        upper.ctx.set_peer(0, lower.ctx.peer_export(), ipc=False)
 
     def step(self, k: int) -> None:
         import torch
@@ -92,6 +117,9 @@ class StripRollout:
             self._step(k, self.stream.cuda_stream)
 
     def _step(self, k: int, stream: int) -> None:
+        if self.transport == "peer":
+            self.ctx.peer_step(k, self.mode, stream)
+            return
         r0, r1 = self.row0, self.row0 + self.rows
         lo_end = min(r1, r0 + HALO) if self.rank > 0 else r0
         hi_beg = max(lo_end, r1 - HALO) if self.rank < self.world - 1 else r1
