@@ -312,7 +312,7 @@ def run_ours(args, world, rank, local):
         scene = configs.make_scene(cfg, 0, xl.astype(np.float64), row0=g0)
         params = configs.make_params(cfg.seed, cfg.hidden8)
         sr = strips.StripRollout(scene, params, xl, np.zeros_like(xl), rank, world, local,
-                                 mode=mode)
+                                 mode=mode, transport=args.transport if mode == "fast" else "nccl")
         nodes_rank = rows * cfg.n
         for k in range(args.warmup):
             sr.step(k)
@@ -344,7 +344,9 @@ def run_ours(args, world, rank, local):
         conf = {"workload": "cfg4: " + cfg.description, "grid": "8192x8192",
                 "nodes_per_gpu": nodes_rank, "timesteps_per_step": 1, "mode": mode,
                 "l2": "no flush: state 2 x %.0f MB >> 126 MB L2" % (24e-6 * nodes_rank),
-                "parallelism": "%d row strips, 2-row halo per step over NCCL" % world}
+                "parallelism": "%d row strips, 2-row halo per step %s" % (
+                    world, "stored into the neighbours' ghost rows over peer memory (fused)"
+                    if sr.transport == "peer" else "over NCCL")}
         scaling = "strong"
     else:
         raise SystemExit("--config must be 2, 4 or 5")
@@ -403,6 +405,8 @@ def main():
     ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
     ap.add_argument("--config", type=int, choices=[2, 4, 5], default=CONFIG_ID)
     ap.add_argument("--e2e-calls", type=int, default=2)
+    ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
+                    help="config 4 halo exchange: NCCL send/recv or the fused peer-store kernel")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=150.0,

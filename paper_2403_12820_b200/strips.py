@@ -82,7 +82,7 @@ class StripRollout:
         if transport == "peer" and mode != "fast":
             raise ValueError("transport 'peer' runs the FAST kernel")
         self.rank, self.world, self.group, self.mode = rank, world, group, mode
-        self.transport = transport
+        self.transport = transport if world > 1 else "nccl"  # one strip: nothing to exchange
         self.ny = scene.ny
         self.row0, self.rows = strip_bounds(scene.ny, world, rank)
         self.g0, self.g1 = local_window(scene.ny, self.row0, self.rows)
