@@ -262,6 +262,23 @@ sc_status sc_trainer_run(sc_trainer* trainer, const sc_train_config* cfg,
                          const sc_params* resume_params, const uint8_t* resume_trainable,
                          sc_adam_state* opt_inout, sc_params* params_out, uint8_t* trainable_out,
                          double* history_out, double* brackets_out);
+/* Data-parallel compute_loss in parts (one rank's contiguous share [b0, b1) of the current
+ * batch), exact when combined in transition order (see training.DistributedTrainer):
+ *   part_forward : cell impulses, residuals and per-node loss terms of the part; the part's data
+ *                  count; bad_out = {first transition with a non-finite impulse, its node} or -1
+ *   part_chain   : the loss sums continued from sums_in = {phys_sq, data_sq} over the part;
+ *                  bad_out = first transition after which a sum is non-finite, or -1
+ *   part_backward: with the batch-wide data count and batch size, the per-transition gradient
+ *                  totals per_b[(b - b0) * 53 + s] (sum them in transition order)
+ *   diagnose_forward: the reference's "network impulse non-finite ..." text for (frame, node). */
+sc_status sc_trainer_part_forward(sc_trainer* trainer, const sc_params* params, int32_t b0,
+                                  int32_t b1, uint64_t* count_out, int32_t* bad_out);
+sc_status sc_trainer_part_chain(sc_trainer* trainer, const double* sums_in, double* sums_out,
+                                int32_t* bad_out);
+sc_status sc_trainer_part_backward(sc_trainer* trainer, const sc_params* params, double alpha,
+                                   uint64_t global_count, int32_t global_batch, double* per_b);
+sc_status sc_trainer_diagnose_forward(sc_trainer* trainer, const sc_params* params, int32_t frame,
+                                      int32_t node, char* msg, int32_t len);
 /* backward_gradients (net.cpp:144-201) for one state and upstream cotangent [node][3]. */
 sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double* x,
                                 const double* v, const sc_params* params, const double* upstream,

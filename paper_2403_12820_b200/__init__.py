@@ -22,6 +22,7 @@ from .training import (AdamState, DeConfig, LossRow, LossValue, ParamGradients, 
                     ScheduleConfig, ScheduleKind, TrainConfig, Trainer, TrainResult,
                     backward_gradients, gradient_check, sample_indices, train,
                        train_loop)
+from .dist_train import CudaPart, DistributedTrainer  # noqa: E402
 from .trajio import (Checkpoint, EvalReport, evaluate, export_obj, load_checkpoint,  # noqa: E402
                      load_trajectory, save_checkpoint, save_trajectory, write_eval_csv,
                      write_loss_csv)
@@ -35,7 +36,7 @@ __all__ = [
     "benchmark_sim", "simulate", "step_semi_implicit", "total_force", "total_impulse",
     "EvalReport", "evaluate", "export_obj", "load_trajectory", "pinned_empty", "save_trajectory",
     "write_eval_csv", "Checkpoint", "load_checkpoint", "save_checkpoint", "write_loss_csv",
-    "AdamState", "DeConfig", "LossRow", "LossValue", "ParamGradients",
+    "AdamState", "CudaPart", "DistributedTrainer", "DeConfig", "LossRow", "LossValue", "ParamGradients",
     "ScheduleConfig", "ScheduleKind", "TrainConfig", "Trainer", "TrainResult",
     "backward_gradients", "gradient_check", "sample_indices", "train", "train_loop",
 ]

@@ -151,6 +151,11 @@ SIGNATURES = {
     "sc_trainer_compute_loss": (C.c_int, [_P, C.POINTER(sc_params), C.c_double, _P, _P]),
     "sc_trainer_run": (C.c_int, [_P, C.POINTER(sc_train_config), C.POINTER(sc_params), _P,
                                  C.POINTER(sc_adam_state), C.POINTER(sc_params), _P, _P, _P]),
+    "sc_trainer_part_forward": (C.c_int, [_P, C.POINTER(sc_params), _I, _I, _P, _P]),
+    "sc_trainer_part_chain": (C.c_int, [_P, _P, _P, _P]),
+    "sc_trainer_part_backward": (C.c_int, [_P, C.POINTER(sc_params), C.c_double, C.c_uint64, _I,
+                                           _P]),
+    "sc_trainer_diagnose_forward": (C.c_int, [_P, C.POINTER(sc_params), _I, _I, C.c_char_p, _I]),
     "sc_backward_gradients": (C.c_int, [C.c_int, _I, _I, _P, _P, C.POINTER(sc_params), _P, _P]),
     "sc_benchmark_launches": (C.c_int, [_P, _I, _I, C.c_int, _P]),
     "sc_ctx_set_strip": (C.c_int, [_P, _I, _I]),

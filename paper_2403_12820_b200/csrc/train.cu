@@ -23,6 +23,7 @@
 #include <array>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <random>
@@ -333,7 +334,7 @@ constexpr int kChainTile = 1024;
 __global__ void __launch_bounds__(256) loss_chain_kernel(const double* __restrict__ pt,
                                                          const double* __restrict__ dt,
                                                          int batch, int64_t n, double* out,
-                                                         int32_t* bad_b) {
+                                                         int32_t* bad_b, double ps0, double ds0) {
   __shared__ double buf[2][2][kChainTile];
   __shared__ int bad_s[2];
   const int64_t total = static_cast<int64_t>(batch) * n;
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(256) loss_chain_kernel(const double* __restric
   load(0);
   __syncthreads();
   const bool consumer = warp < 2 && lane == 0;
-  double acc = 0.0;
+  double acc = warp == 0 ? ps0 : ds0;  // a rank continues the chain where the previous one ended
   int bad = kNone;
   int b = 0;
   int64_t boundary = n;  // global index one past batch element b
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(256) bwd_reduce_kernel(const double* __restric
 // total.add_scaled(partial, 1.0) over chunks (net.cpp:198-199), then grads.add_scaled(g, 1.0)
 // over batch elements (train.cpp:205); `grads` carries the running sum across groups.
 __global__ void bwd_final_kernel(const double* __restrict__ partial, int nb, int chunks,
-                                 double* __restrict__ grads) {
+                                 double* __restrict__ grads, double* __restrict__ per_b) {
   const int s = threadIdx.x;
   if (s >= kScalars) return;
   double g = grads[s];
@@ -603,6 +604,7 @@ __global__ void bwd_final_kernel(const double* __restrict__ partial, int nb, int
       if (k0 + u >= total) break;
       tot = R::add(tot, R::mul(v[u], 1.0));
       if (++c == chunks) {
+        if (per_b) per_b[((k0 + u) / chunks) * kScalars + s] = tot;  // this element's total
         g = R::add(g, R::mul(tot, 1.0));
         tot = 0.0;
         c = 0;
@@ -741,6 +743,9 @@ struct sc_trainer {
     double* host = nullptr;  // pinned: {phys_sq, data_sq, first bad element (as double)}
   };
   std::deque<ChainSlot> slots;  // stable addresses as slots are added
+  // a part [part_b0, part_b0 + part_nb) of the current batch (sc_trainer_part_*): one rank's
+  // share of a data-parallel compute_loss
+  int part_b0 = 0, part_nb = 0;
   double* slot_host = nullptr;
   ~sc_trainer() {
     for (ChainSlot& c : slots) {
@@ -922,7 +927,8 @@ LossLaunch launch_loss(sc_trainer* t, const sc_params& params, Batch& bt, double
   ck(cudaGetLastError(), "loss_fwd_kernel");
   ck(cudaEventRecord(slot.ev_in, t->s0), "event");
   ck(cudaStreamWaitEvent(slot.st, slot.ev_in, 0), "wait");
-  loss_chain_kernel<<<1, 256, 0, slot.st>>>(slot.pt.p, slot.dtm.p, B, n, slot.out.p, slot.bad.p);
+  loss_chain_kernel<<<1, 256, 0, slot.st>>>(slot.pt.p, slot.dtm.p, B, n, slot.out.p, slot.bad.p,
+                                            0.0, 0.0);
   ck(cudaGetLastError(), "loss_chain_kernel");
   ck(cudaMemcpyAsync(slot.host, slot.out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, slot.st),
      "D2H chain");
@@ -960,7 +966,7 @@ LossLaunch launch_loss(sc_trainer* t, const sc_params& params, Batch& bt, double
       ck(cudaGetLastError(), "bwd_terms_kernel");
       bwd_reduce_kernel<<<nbat * chunks, 256, 0, t->s0>>>(t->terms.p, n, chunks, t->partial.p);
       ck(cudaGetLastError(), "bwd_reduce_kernel");
-      bwd_final_kernel<<<1, 64, 0, t->s0>>>(t->partial.p, nbat, chunks, t->grads.p);
+      bwd_final_kernel<<<1, 64, 0, t->s0>>>(t->partial.p, nbat, chunks, t->grads.p, nullptr);
       ck(cudaGetLastError(), "bwd_final_kernel");
     }
   }
@@ -1319,6 +1325,160 @@ sc_status sc_trainer_compute_loss(sc_trainer* t, const sc_params* params, double
   });
 }
 
+// ---- data-parallel compute_loss in parts (one per rank) ------------------------------------
+// compute_loss over B transitions split into contiguous parts is exactly the single-device
+// result when (i) the data count is summed over parts before the backward pass, (ii) the loss
+// chain runs part after part, each starting from the previous part's running sums, and (iii)
+// the per-transition gradient totals are summed in transition order (train.cpp:205). These
+// entry points run one part; the caller (training.DistributedTrainer) does the exchanges.
+
+sc_status sc_trainer_part_forward(sc_trainer* t, const sc_params* params, int32_t b0, int32_t b1,
+                                  uint64_t* count_out, int32_t* bad_out) {
+  return guarded([&] {
+    if (!t) fail(SC_ERR_STATE, "null trainer");
+    if (!params || !count_out || !bad_out) fail(SC_ERR_CONFIG, "part: null argument");
+    const int B = static_cast<int>(t->batch.idx.size());
+    if (B == 0) fail(SC_ERR_CONFIG, "compute_loss: empty batch");
+    if (b0 < 0 || b1 > B || b0 >= b1) fail(SC_ERR_CONFIG, "part: bad transition range");
+    if (!(params->isru_alpha > 0.0)) fail(SC_ERR_CONFIG, "isru_alpha: must be > 0");
+    ck(cudaSetDevice(t->device), "cudaSetDevice");
+    const int nb = b1 - b0;
+    const int64_t n = t->n;
+    const size_t bn = static_cast<size_t>(nb) * n;
+    sc_trainer::ChainSlot& slot = chain_slot(t, 0);
+    ck(cudaStreamSynchronize(slot.st), "chain");
+    slot.pt.ensure(bn);
+    slot.dtm.ensure(bn);
+    slot.out.ensure(2);
+    slot.bad.ensure(1);
+    t->rp.ensure(bn * 3);
+    t->rd.ensure(bn * 3);
+    t->count.ensure(1);
+    t->bad_fwd.ensure(nb);
+    ck(cudaMemsetAsync(t->count.p, 0, sizeof(unsigned long long), t->s0), "memset");
+    ck(cudaMemsetAsync(t->bad_fwd.p, 0x7F, sizeof(int32_t) * nb, t->s0), "memset");
+    LossArgs la{};
+    la.fr = Frames{t->fx.p, t->fv.p, t->batch.idx_d.p + b0, t->nx, t->ny, n};
+    la.batch = nb;
+    la.force_dt = t->batch.force_dt.p + static_cast<size_t>(b0) * n * 3;
+    la.inv_mass = 1.0 / t->mass;
+    la.net = net_of(*params);
+    la.sa.spheres = static_cast<const SphereConst<double>*>(t->view.spheres);
+    la.sa.planes = static_cast<const PlaneConst<double>*>(t->view.planes);
+    la.sa.pin_bits = t->view.pin_bits;
+    la.sa.pin_rank = t->view.pin_rank;
+    la.sa.pin_anchors = static_cast<const double*>(t->view.anchors);
+    la.cloth = static_cast<const ClothConst<double>*>(t->view.cloths);
+    la.rp = t->rp.p;
+    la.rd = t->rd.p;
+    la.phys_term = slot.pt.p;
+    la.data_term = slot.dtm.p;
+    la.data_count = t->count.p;
+    la.bad_fwd = t->bad_fwd.p;
+    loss_fwd_kernel<<<grid_for(static_cast<int64_t>(bn)), 256, 0, t->s0>>>(la);
+    ck(cudaGetLastError(), "loss_fwd_kernel");
+    std::vector<int32_t> bad(static_cast<size_t>(nb));
+    unsigned long long cnt = 0;
+    ck(cudaMemcpyAsync(&cnt, t->count.p, sizeof cnt, cudaMemcpyDeviceToHost, t->s0), "D2H");
+    ck(cudaMemcpyAsync(bad.data(), t->bad_fwd.p, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost,
+                       t->s0),
+       "D2H");
+    ck(cudaStreamSynchronize(t->s0), "part forward");
+    t->part_b0 = b0;
+    t->part_nb = nb;
+    *count_out = cnt;
+    bad_out[0] = -1;  // first transition (global index) with a non-finite impulse, and its node
+    bad_out[1] = -1;
+    for (int b = 0; b < nb; ++b)
+      if (bad[static_cast<size_t>(b)] != kNone) {
+        bad_out[0] = b0 + b;
+        bad_out[1] = bad[static_cast<size_t>(b)];
+        break;
+      }
+  });
+}
+
+sc_status sc_trainer_part_chain(sc_trainer* t, const double* sums_in, double* sums_out,
+                                int32_t* bad_out) {
+  return guarded([&] {
+    if (!t || t->part_nb == 0) fail(SC_ERR_STATE, "part chain: no part forward pass");
+    if (!sums_in || !sums_out || !bad_out) fail(SC_ERR_CONFIG, "part: null argument");
+    ck(cudaSetDevice(t->device), "cudaSetDevice");
+    sc_trainer::ChainSlot& slot = chain_slot(t, 0);
+    loss_chain_kernel<<<1, 256, 0, t->s0>>>(slot.pt.p, slot.dtm.p, t->part_nb, t->n, slot.out.p,
+                                            slot.bad.p, sums_in[0], sums_in[1]);
+    ck(cudaGetLastError(), "loss_chain_kernel");
+    int32_t bad = kNone;
+    ck(cudaMemcpyAsync(sums_out, slot.out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, t->s0),
+       "D2H");
+    ck(cudaMemcpyAsync(&bad, slot.bad.p, sizeof bad, cudaMemcpyDeviceToHost, t->s0), "D2H");
+    ck(cudaStreamSynchronize(t->s0), "part chain");
+    *bad_out = bad == kNone ? -1 : t->part_b0 + bad;
+  });
+}
+
+sc_status sc_trainer_part_backward(sc_trainer* t, const sc_params* params, double alpha,
+                                   uint64_t global_count, int32_t global_batch, double* per_b) {
+  return guarded([&] {
+    if (!t || t->part_nb == 0) fail(SC_ERR_STATE, "part backward: no part forward pass");
+    if (!params || !per_b) fail(SC_ERR_CONFIG, "part: null argument");
+    ck(cudaSetDevice(t->device), "cudaSetDevice");
+    const int nb = t->part_nb;
+    const int64_t n = t->n;
+    const unsigned long long cnt = global_count;
+    ck(cudaMemcpyAsync(t->count.p, &cnt, sizeof cnt, cudaMemcpyHostToDevice, t->s0), "H2D");
+    const int free_count = static_cast<int>(n) - t->n_pins;
+    const double phys_denom = 3.0 * static_cast<double>(global_batch) * free_count;
+    const int chunks = static_cast<int>((n + kChunk - 1) / kChunk);
+    const size_t per_elem = static_cast<size_t>(chunks) * kTerms * kChunk * sizeof(double);
+    const int group = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(static_cast<size_t>(nb), t->term_budget / per_elem)));
+    t->terms.ensure(static_cast<size_t>(group) * chunks * kTerms * kChunk);
+    t->partial.ensure(static_cast<size_t>(group) * chunks * kScalars);
+    t->grads.ensure(kScalars);
+    DBuf<double> pb;
+    pb.ensure(static_cast<size_t>(nb) * kScalars);
+    ck(cudaMemsetAsync(t->grads.p, 0, sizeof(double) * kScalars, t->s0), "memset");
+    const Frames fr{t->fx.p, t->fv.p, t->batch.idx_d.p + t->part_b0, t->nx, t->ny, n};
+    for (int g0 = 0; g0 < nb; g0 += group) {
+      const int ng = std::min(group, nb - g0);
+      BwdArgs ba{};
+      ba.fr = fr;
+      ba.b0 = g0;
+      ba.nb = ng;
+      ba.net = net_of(*params);
+      ba.rp = t->rp.p;
+      ba.rd = t->rd.p;
+      ba.phys_coeff = free_count > 0 ? 2.0 * alpha / phys_denom : 0.0;
+      ba.alpha_loss = alpha;
+      ba.data_count = t->count.p;
+      ba.terms = t->terms.p;
+      ba.chunks = chunks;
+      bwd_terms_kernel<<<grid_for(n * ng), 256, 0, t->s0>>>(ba);
+      ck(cudaGetLastError(), "bwd_terms_kernel");
+      bwd_reduce_kernel<<<ng * chunks, 256, 0, t->s0>>>(t->terms.p, n, chunks, t->partial.p);
+      ck(cudaGetLastError(), "bwd_reduce_kernel");
+      bwd_final_kernel<<<1, 64, 0, t->s0>>>(t->partial.p, ng, chunks, t->grads.p,
+                                            pb.p + static_cast<size_t>(g0) * kScalars);
+      ck(cudaGetLastError(), "bwd_final_kernel");
+    }
+    ck(cudaMemcpyAsync(per_b, pb.p, sizeof(double) * nb * kScalars, cudaMemcpyDeviceToHost,
+                       t->s0),
+       "D2H");
+    ck(cudaStreamSynchronize(t->s0), "part backward");
+  });
+}
+
+sc_status sc_trainer_diagnose_forward(sc_trainer* t, const sc_params* params, int32_t frame,
+                                      int32_t node, char* msg, int32_t len) {
+  return guarded([&] {
+    if (!t || !params || !msg || len < 1) fail(SC_ERR_CONFIG, "diagnose: null argument");
+    ck(cudaSetDevice(t->device), "cudaSetDevice");
+    const std::string m = diagnose_forward(t, frame, node, *params);
+    std::snprintf(msg, static_cast<size_t>(len), "%s", m.c_str());
+  });
+}
+
 sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double* x,
                                 const double* v, const sc_params* params, const double* upstream,
                                 double* grads_out) {
@@ -1356,7 +1516,7 @@ sc_status sc_backward_gradients(int device, int32_t nx, int32_t ny, const double
     ck(cudaGetLastError(), "bwd_terms_kernel");
     bwd_reduce_kernel<<<chunks, 256>>>(terms.p, n, chunks, partial.p);
     ck(cudaGetLastError(), "bwd_reduce_kernel");
-    bwd_final_kernel<<<1, 64>>>(partial.p, 1, chunks, grads.p);
+    bwd_final_kernel<<<1, 64>>>(partial.p, 1, chunks, grads.p, nullptr);
     ck(cudaGetLastError(), "bwd_final_kernel");
     ck(cudaMemcpy(grads_out, grads.p, sizeof(double) * kScalars, cudaMemcpyDeviceToHost), "D2H");
   });

@@ -315,6 +315,24 @@ class Rng:
     def uniform(self, lo: float, hi: float) -> float:
         return lo + (hi - lo) * self.uniform01()
 
+    def uniform_below(self, n: int) -> int:
+        """Rejection-sampled uniform integer in [0, n) (rng.hpp:20-27)."""
+        m = 0xFFFFFFFFFFFFFFFF
+        limit = m - m % n
+        while True:
+            r = self.next_u64()
+            if r < limit:
+                return r % n
+
+    @staticmethod
+    def mix(seed: int, stream: int) -> int:
+        """Rng::mix (rng.hpp:36-42), splitmix64 finaliser over the pair."""
+        m = 0xFFFFFFFFFFFFFFFF
+        z = (seed + 0x9E3779B97F4A7C15 * (stream + 1)) & m
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+        return z ^ (z >> 31)
+
 
 def gradient_check(nx: int = 8, ny: int = 8, seed: int = 7, eps: float = 1e-6,
                    device: int = 0) -> float:

@@ -220,3 +220,63 @@ def test_train_binding_checkpoint_bytes_match_reference(tmp_path):
     sc.save_checkpoint(pr, rc)
     ours.save_checkpoint(po, ours.Checkpoint(params, None, kw["epochs"], ""))
     assert open(po, "rb").read() == open(pr, "rb").read()
+
+
+def test_distributed_trainer_single_rank_matches_trainer():
+    """DistributedTrainer over the GPU part with one rank = Trainer (compute_loss and run)."""
+    z = load("train_f64")
+    scene, traj = fixture_trainer(z)
+    p = ours.NetworkParams.from_scalars(z["params"])
+    with ours.Trainer(scene, traj) as t:
+        t.set_batch(z["batch_idx"])
+        want, wg = t.compute_loss(p, 0.3)
+        cfg = ours.TrainConfig(alpha=0.5, batch_size=8, epochs=6, seed=3,
+                               de=ours.DeConfig(population=5, generations=2, probe_batch=4))
+        rw = t.run(cfg)
+    part = ours.CudaPart(scene, traj)
+    d = ours.DistributedTrainer(part)
+    d.set_batch(z["batch_idx"])
+    got, gg = d.compute_loss(p, 0.3)
+    assert bits([got.total, got.physics, got.data], [want.total, want.physics, want.data])
+    assert bits(gg.flat, wg.flat)
+    r = d.run(cfg)
+    assert bits(r.params.scalars(), rw.params.scalars())
+    assert r.params.brackets == rw.params.brackets
+    assert bits([[h.step, h.lr, h.physics, h.data, h.total] for h in r.history],
+                [[h.step, h.lr, h.physics, h.data, h.total] for h in rw.history])
+    part.close()
+
+
+def test_parts_combine_exactly():
+    """Two GPU parts of one batch (two ranks emulated in one process, one after the other):
+    count summed, loss chain handed over, per-transition gradients summed in order — equal to
+    the single-part compute_loss bit for bit."""
+    z = load("train_f64")
+    scene, traj = fixture_trainer(z)
+    p = ours.NetworkParams.from_scalars(z["params"])
+    idx = list(z["batch_idx"])
+    B, m = len(idx), 7
+    with ours.Trainer(scene, traj) as t:
+        t.set_batch(idx)
+        want, wg = t.compute_loss(p, 0.3)
+    a, b = ours.CudaPart(scene, traj), ours.CudaPart(scene, traj)
+    a.set_batch(idx)
+    b.set_batch(idx)
+    ca, bad_a, _ = a.forward(p, 0, m)
+    cb, bad_b, _ = b.forward(p, m, B)
+    assert bad_a < 0 and bad_b < 0
+    ps, ds, bl = a.chain(0.0, 0.0)
+    ps, ds, bl2 = b.chain(ps, ds)
+    assert bl < 0 and bl2 < 0
+    count = ca + cb
+    per_b = np.concatenate([a.backward(p, 0.3, count, B, m), b.backward(p, 0.3, count, B, B - m)])
+    g = [0.0] * 53
+    for row in per_b.tolist():
+        g = [g[s] + row[s] * 1.0 for s in range(53)]
+    assert bits(g, wg.flat)
+    free = scene.nx * scene.ny - len(scene.bc.nodes)
+    physics = ps / (3.0 * B * free)
+    data = ds / (6.0 * count)
+    assert bits([physics, data], [want.physics, want.data])
+    a.close()
+    b.close()
