@@ -1131,7 +1131,7 @@ sc_status sc_benchmark_launches(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mo
   });
 }
 
-int64_t sc_ctx_halo_elems(sc_ctx* c) { return c ? static_cast<int64_t>(6) * 2 * c->nx : 0; }
+int64_t sc_ctx_halo_elems(sc_ctx* c) { return c ? static_cast<int64_t>(6) * 2 * c->pitch : 0; }
 
 }  // extern "C"
 
@@ -1149,15 +1149,16 @@ void halo_copy(sc_ctx* c, int side, void* dev, bool pack, cudaStream_t st) {
   const size_t e = c->elem();
   const int64_t S = c->plane_stride;
   unsigned char* buf = static_cast<unsigned char*>(c->state[1 - c->cur]);
-  // halo buffer [2 rows][x.xy 2nx | v.xy 2nx | x.z nx | v.z nx] = 6*nx elements per row
+  // halo buffer [2 rows][x.xy 2p | v.xy 2p | x.z p | v.z p] = 6*pitch elements per row (whole
+  // rows in the device layout, swizzle included)
   for (int r = 0; r < 2; ++r) {
     const int g = grow + r;
     if (g < 0 || g >= c->ny) continue;
     const int64_t lr = g - c->g0;
     const int64_t seg_off[4] = {elem_index(0, lr, 0, c->pitch, S), elem_index(3, lr, 0, c->pitch, S),
                                 elem_index(2, lr, 0, c->pitch, S), elem_index(5, lr, 0, c->pitch, S)};
-    const int64_t seg_len[4] = {2LL * c->nx, 2LL * c->nx, c->nx, c->nx};
-    int64_t hoff = static_cast<int64_t>(r) * 6 * c->nx;
+    const int64_t seg_len[4] = {2LL * c->pitch, 2LL * c->pitch, c->pitch, c->pitch};
+    int64_t hoff = static_cast<int64_t>(r) * 6 * c->pitch;
     for (int q = 0; q < 4; ++q) {
       unsigned char* st_ptr = buf + seg_off[q] * e;
       unsigned char* h_ptr = static_cast<unsigned char*>(dev) + hoff * e;

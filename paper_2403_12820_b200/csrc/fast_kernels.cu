@@ -142,7 +142,10 @@ __device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, V dx, V d
 }
 
 // Lane windows of a staged row: columns ix0-2 .. ix0+5 <-> box column 4*lane+2 .. 4*lane+9,
-// columns ix0 .. ix0+3 <-> 4*lane+4 .. 4*lane+7.
+// columns ix0 .. ix0+3 <-> 4*lane+4 .. 4*lane+7. The (x, y) planes carry the xy_col swizzle
+// (sc_device.cuh): box column j of a strip (x0 a multiple of 128, box from x0-4) sits at
+// position xsw(j); a lane's four 2-column pieces are at xsw(4 lane + 2 + 2q), q = 0..3.
+__device__ __forceinline__ int xsw(int j) { return j ^ (((j + 28) >> 3) & 2); }
 __device__ __forceinline__ void win8(const float* zplane, int lane, float* o) {
   const float2 l = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
   const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
@@ -150,10 +153,9 @@ __device__ __forceinline__ void win8(const float* zplane, int lane, float* o) {
   o[0] = l.x; o[1] = l.y; o[2] = m.x; o[3] = m.y; o[4] = m.z; o[5] = m.w; o[6] = r.x; o[7] = r.y;
 }
 __device__ __forceinline__ void win8(const float* xyplane, int lane, float2* o) {
-  const float4* p = reinterpret_cast<const float4*>(xyplane + 2 * (FW * lane + 2));
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float4 m = p[q];
+    const float4 m = *reinterpret_cast<const float4*>(xyplane + 2 * xsw(FW * lane + 2 + 2 * q));
     o[2 * q] = make_float2(m.x, m.y);
     o[2 * q + 1] = make_float2(m.z, m.w);
   }
@@ -163,8 +165,8 @@ __device__ __forceinline__ void win4(const float* zplane, int lane, float* o) {
   o[0] = m.x; o[1] = m.y; o[2] = m.z; o[3] = m.w;
 }
 __device__ __forceinline__ void win4(const float* xyplane, int lane, float2* o) {
-  const float4* p = reinterpret_cast<const float4*>(xyplane + 2 * (FW * lane + 4));
-  const float4 a = p[0], b = p[1];
+  const float4 a = *reinterpret_cast<const float4*>(xyplane + 2 * xsw(FW * lane + 4));
+  const float4 b = *reinterpret_cast<const float4*>(xyplane + 2 * xsw(FW * lane + 6));
   o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w);
   o[2] = make_float2(b.x, b.y); o[3] = make_float2(b.z, b.w);
 }
@@ -462,7 +464,7 @@ __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, co
 
 // component d of x (X = true) or v at box column j of a ring slot
 __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int j) {
-  return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * j + d] : slot[(X ? Z_X : Z_V) + j];
+  return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * xsw(j) + d] : slot[(X ? Z_X : Z_V) + j];
 }
 
 // One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
@@ -639,10 +641,15 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
         }
         float* ovxy = oxy + 2 * S;
-        reinterpret_cast<float4*>(oxy)[0] = make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
-        reinterpret_cast<float4*>(oxy)[1] = make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
-        reinterpret_cast<float4*>(ovxy)[0] = make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
-        reinterpret_cast<float4*>(ovxy)[1] = make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
+        const int sw = (ix0 >> 3) & 2;  // xy_col: this lane's group stores its halves swapped
+        *reinterpret_cast<float4*>(oxy + 2 * sw) =
+            make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
+        *reinterpret_cast<float4*>(oxy + 2 * (2 ^ sw)) =
+            make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
+        *reinterpret_cast<float4*>(ovxy + 2 * sw) =
+            make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
+        *reinterpret_cast<float4*>(ovxy + 2 * (2 ^ sw)) =
+            make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
         *reinterpret_cast<float4*>(oz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
         *reinterpret_cast<float4*>(oz + S) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         // fused halo exchange: the two owned rows at a peer side also go into the neighbour's
@@ -658,11 +665,14 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           float* pb = po + static_cast<int64_t>(b) * 6 * S2;
           float* pxy = pb + 2 * (lr2 * a.pitch + ix0);
           float* pz = pb + 4 * S2 + lr2 * a.pitch + ix0;
-          reinterpret_cast<float4*>(pxy)[0] = make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
-          reinterpret_cast<float4*>(pxy)[1] = make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
-          reinterpret_cast<float4*>(pxy + 2 * S2)[0] =
+          const int sw2 = (ix0 >> 3) & 2;
+          *reinterpret_cast<float4*>(pxy + 2 * sw2) =
+              make_float4(xo[0][0], xo[1][0], xo[0][1], xo[1][1]);
+          *reinterpret_cast<float4*>(pxy + 2 * (2 ^ sw2)) =
+              make_float4(xo[0][2], xo[1][2], xo[0][3], xo[1][3]);
+          *reinterpret_cast<float4*>(pxy + 2 * S2 + 2 * sw2) =
               make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
-          reinterpret_cast<float4*>(pxy + 2 * S2)[1] =
+          *reinterpret_cast<float4*>(pxy + 2 * S2 + 2 * (2 ^ sw2)) =
               make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
           *reinterpret_cast<float4*>(pz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
           *reinterpret_cast<float4*>(pz + S2) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);

@@ -26,17 +26,26 @@ __host__ __device__ constexpr int off_dy(int c) {
        : c == 6 ? -1 : c == 7 ? -1 : c == 8 ? 0 : c == 9 ? 2 : c == 10 ? 0 : -2;
 }
 
+// Column swizzle of the interleaved (x, y) planes: within every aligned group of 4 columns whose
+// group index has bit 2 set (columns with bit 4 set), the two 2-column halves are swapped. A
+// FAST-kernel lane owns one group; with this layout the lanes of a quarter-warp read their
+// 16-byte window pieces from 8 distinct bank groups (the plain layout puts lanes l and l+4 on
+// the same banks). Pure permutation within a group: any row segment of whole groups is
+// contiguous, and every access goes through elem_index / xy_col.
+__host__ __device__ __forceinline__ int64_t xy_col(int64_t c) { return c ^ ((c >> 3) & 2); }
+
 // Element index of component p (0..5 = x.x x.y x.z v.x v.y v.z) of local row r, column c
 // within one cloth's block (see the layout above).
 __host__ __device__ __forceinline__ int64_t elem_index(int p, int64_t r, int64_t c, int64_t pitch,
                                                        int64_t S) {
   const int64_t rc = r * pitch + c;
+  const int64_t rx = r * pitch + xy_col(c);
   switch (p) {
-    case 0: return 2 * rc;
-    case 1: return 2 * rc + 1;
+    case 0: return 2 * rx;
+    case 1: return 2 * rx + 1;
     case 2: return 4 * S + rc;
-    case 3: return 2 * S + 2 * rc;
-    case 4: return 2 * S + 2 * rc + 1;
+    case 3: return 2 * S + 2 * rx;
+    case 4: return 2 * S + 2 * rx + 1;
     default: return 5 * S + rc;
   }
 }
