@@ -117,27 +117,33 @@ __device__ __forceinline__ float2 vrsq(float2 q) { return make_float2(rsqrt_q(q.
 // Edge contribution to its origin node a (channel ca) and far node b (channel cb = -ca):
 //   a: acc += dx*wL'_ca + s*(wN'_ca + dv*wD'_ca)
 //   b: acc += dx*(-wL'_cb) + s*(dv*wD'_cb - wN'_cb)
-// with dx = x_a - x_b, dv = v_a - v_b, s = dx * rsqrt(1 + alpha'_c dx^2) and the gains folded
-// into the primed weights (wL' = g wL, wN' = g wN, wD' = g^2 wD, alpha' = alpha g^2).
-// Invalid edges (an endpoint outside the grid) arrive with dx = dv = 0 and contribute exactly 0.
+// with dx = x_a - x_b, dv = v_a - v_b, s = dx * r, r = rsqrt(1 + alpha'_c dx^2) and the gains
+// folded into the primed weights (wL' = g wL, wN' = g wN, wD' = g^2 wD, alpha' = alpha g^2).
+// Evaluated folded, acc += dx * (wL' + r * (wN' + dv wD')): three FMAs per endpoint and no
+// shared s = dx * r product. Invalid edges (an endpoint outside the grid) arrive with dx = 0
+// and contribute exactly 0 whatever dv is (w stays finite), so only dx is masked.
 template <bool ALPHA1, bool PA, bool PB, typename V>
 __device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, V dx, V dv, V& acc_a,
                                      V& acc_b) {
   const V q = ALPHA1 ? vq(dx) : vqa(dx, f.alpha[ca]);
-  const V s = vmul(dx, vrsq(q));
+  const V r = vrsq(q);
   if (PA) {
     const V t = vfma(dv, f.wd[ca], [&] {
       if constexpr (sizeof(V) == 8) return vsplat2(f.wn[ca]); else return vsplat(f.wn[ca]);
     }());
-    acc_a = vfma(dx, f.wl[ca], acc_a);
-    acc_a = vfmav(s, t, acc_a);
+    const V w = vfmav(r, t, [&] {
+      if constexpr (sizeof(V) == 8) return vsplat2(f.wl[ca]); else return vsplat(f.wl[ca]);
+    }());
+    acc_a = vfmav(dx, w, acc_a);
   }
   if (PB) {
     const V t = vfma(dv, f.wd[cb], [&] {
       if constexpr (sizeof(V) == 8) return vsplat2(f.nwn[cb]); else return vsplat(f.nwn[cb]);
     }());
-    acc_b = vfma(dx, f.nwl[cb], acc_b);
-    acc_b = vfmav(s, t, acc_b);
+    const V w = vfmav(r, t, [&] {
+      if constexpr (sizeof(V) == 8) return vsplat2(f.nwl[cb]); else return vsplat(f.nwl[cb]);
+    }());
+    acc_b = vfmav(dx, w, acc_b);
   }
 }
 
@@ -205,7 +211,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
       V dx = vsub(x1[e + 1], xr[e + 2]), dv = vsub(v1[e + 1], vr[e + 2]);
       if (e == 4) {
         dx = vscale(dx, mRt);
-        dv = vscale(dv, mRt);
       }
       edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[e - 1], dummy);
     }
@@ -214,7 +219,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
       V dx = vsub(x1[e + 2], xr[e + 1]), dv = vsub(v1[e + 2], vr[e + 1]);
       if (e == 0) {
         dx = vscale(dx, mL);
-        dv = vscale(dv, mL);
       }
       edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[e], dummy);
     }
@@ -231,7 +235,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     if (e == 0 || e == 4) {
       const float m = e == 0 ? mL : mRt;
       dx = vscale(dx, m);
-      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, A2[3], dummy);
@@ -244,7 +247,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     if (e <= 1 || e >= 4) {
       const float m = e <= 1 ? mL : mRt;
       dx = vscale(dx, m);
-      dv = vscale(dv, m);
     }
     if (e <= 1) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy, A2[e]);
     else if (e >= 4) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[e - 2], dummy);
@@ -258,7 +260,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     V dx2 = vsub(x2[k], xr[k + 2]), dv2 = vsub(v2[k], vr[k + 2]);
     if (GENERAL) {
       dx2 = vscale(dx2, m2);
-      dv2 = vscale(dv2, m2);
     }
     edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[k], A2[k]);
   }
@@ -270,7 +271,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     V dx = vsub(x1[k + 2], xr[k + 2]), dv = vsub(v1[k + 2], vr[k + 2]);
     if (GENERAL) {
       dx = vscale(dx, m1);
-      dv = vscale(dv, m1);
     }
     edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[k], A2[k]);
   }
@@ -281,7 +281,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     if (GENERAL || e == 0 || e == 4) {
       const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
       dx = vscale(dx, m);
-      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[3], dummy);
@@ -294,7 +293,6 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     if (GENERAL || e == 0 || e == 4) {
       const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
       dx = vscale(dx, m);
-      dv = vscale(dv, m);
     }
     if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[0], dummy);
     else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, A2[3]);
@@ -352,7 +350,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
       float dx = zw(x1, e + 1) - zw(xr, e + 2), dv = zw(v1, e + 1) - zw(vr, e + 2);
       if (e == 4) {
         dx *= mRt;
-        dv *= mRt;
       }
       edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, e - 1), dummy);
     }
@@ -361,7 +358,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
       float dx = zw(x1, e + 2) - zw(xr, e + 1), dv = zw(v1, e + 2) - zw(vr, e + 1);
       if (e == 0) {
         dx *= mL;
-        dv *= mL;
       }
       edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, e), dummy);
     }
@@ -378,7 +374,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     if (e == 0 || e == 4) {
       const float m = e == 0 ? mL : mRt;
       dx *= m;
-      dv *= m;
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, zc(A2, 0));
     else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, zc(A2, 3), dummy);
@@ -391,7 +386,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     if (j == 0 || j == 2) {
       const float m = j == 0 ? mL : mRt;
       dx = vscale(dx, m);
-      dv = vscale(dv, m);
     }
     if (j == 0) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy2, A2[0]);
     else if (j == 2) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[1], dummy2);
@@ -405,7 +399,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     float2 dx2 = vsub(x2[j], xr[j + 1]), dv2 = vsub(v2[j], vr[j + 1]);
     if (GENERAL) {
       dx2 = vscale(dx2, m2);
-      dv2 = vscale(dv2, m2);
     }
     edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[j], A2[j]);
   }
@@ -416,7 +409,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     float2 dx = vsub(x1[j + 1], xr[j + 1]), dv = vsub(v1[j + 1], vr[j + 1]);
     if (GENERAL) {
       dx = vscale(dx, m1);
-      dv = vscale(dv, m1);
     }
     edge<ALPHA1, true, true>(f, 1, 3, dx, dv, A1[j], A2[j]);
   }
@@ -427,7 +419,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     if (GENERAL || e == 0 || e == 4) {
       const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
       dx *= m;
-      dv *= m;
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, zc(A2, 0));
     else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, 3), dummy);
@@ -440,7 +431,6 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     if (GENERAL || e == 0 || e == 4) {
       const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
       dx *= m;
-      dv *= m;
     }
     if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, 0), dummy);
     else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, zc(A2, 3));
