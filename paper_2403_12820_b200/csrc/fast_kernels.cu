@@ -667,8 +667,118 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           *reinterpret_cast<float4*>(pz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
           *reinterpret_cast<float4*>(pz + S2) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         }
+      } else if (!cc.plug_pressure) {
+        // colliders and/or the contact mask: the lane's 4 nodes together (collider outer, node
+        // inner: each collider's constants are loaded once per row), each node through the
+        // same IEEE-exact sequence as advance_with_impulse (sc_device.cuh), packed stores
+        float2 xs[4], vs[4];
+        float xz[4], vz[4];
+        win4(row2 + XY_X, lane, xs);
+        win4(row2 + XY_V, lane, vs);
+        win4(row2 + Z_X, lane, xz);
+        win4(row2 + Z_V, lane, vz);
+        float x[4][3], vo[4][3], xo[4][3];
+        uint8_t mk[4];
+        bool fin_imp = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float v[3] = {vs[k].x, vs[k].y, vz[k]};
+          float imp[3] = {P0[k].x, P0[k].y, zc(Z0, k)};
+          fin_imp = fin_imp && isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]);
+          plug_tail(cc, v, imp);
+          x[k][0] = xs[k].x;
+          x[k][1] = xs[k].y;
+          x[k][2] = xz[k];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) vo[k][d] = __fadd_rn(v[d], imp[d]);
+          mk[k] = 0;
+        }
+        if (a.health && !fin_imp) {
+          for (int k = 0; k < 4; ++k)
+            if (!(isfinite(P0[k].x) && isfinite(P0[k].y) && isfinite(zc(Z0, k)))) {
+              const unsigned long long key = (static_cast<unsigned long long>(a.k + 1) << 32) |
+                                             static_cast<unsigned long long>(Rf * nx + ix0 + k);
+              atomicMin(&a.health[b].impulse_key, key);
+              break;
+            }
+        }
+#pragma unroll 1
+        for (int q = 0; q < cc.n_spheres; ++q) {
+          const SphereConst<float> sp = a.spheres[cc.sphere0 + q];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sphere_velocity(sp, x[k], vo[k], mk[k]);
+        }
+#pragma unroll 1
+        for (int q = 0; q < cc.n_planes; ++q) {
+          const PlaneConst<float> pl = a.planes[cc.plane0 + q];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) plane_velocity(pl, x[k], vo[k], mk[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xo[k][d] = __fadd_rn(x[k][d], __fmul_rn(vo[k][d], cc.dt));
+#pragma unroll 1
+        for (int q = 0; q < cc.n_spheres; ++q) {
+          const SphereConst<float> sp = a.spheres[cc.sphere0 + q];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sphere_position(sp, xo[k], vo[k], mk[k]);
+        }
+#pragma unroll 1
+        for (int q = 0; q < cc.n_planes; ++q) {
+          const PlaneConst<float> pl = a.planes[cc.plane0 + q];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) plane_position(pl, xo[k], vo[k], mk[k]);
+        }
+        if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            repin(a, cc, Rf, static_cast<int64_t>(Rf) * nx + ix0 + k, xo[k], vo[k], mk[k]);
+        }
+        if (a.health) {
+          bool fin = true;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) fin = fin && isfinite(xo[k][d]) && isfinite(vo[k][d]);
+          if (!fin) atomicMin(&a.health[b].state_frame, a.k + 1);
+        }
+        const int sw = (ix0 >> 3) & 2;  // xy_col swizzle of this lane's group
+        const float4 xy01 = make_float4(xo[0][0], xo[0][1], xo[1][0], xo[1][1]);
+        const float4 xy23 = make_float4(xo[2][0], xo[2][1], xo[3][0], xo[3][1]);
+        const float4 vxy01 = make_float4(vo[0][0], vo[0][1], vo[1][0], vo[1][1]);
+        const float4 vxy23 = make_float4(vo[2][0], vo[2][1], vo[3][0], vo[3][1]);
+        const float4 z4 = make_float4(xo[0][2], xo[1][2], xo[2][2], xo[3][2]);
+        const float4 vz4 = make_float4(vo[0][2], vo[1][2], vo[2][2], vo[3][2]);
+        float* ovxy = oxy + 2 * S;
+        *reinterpret_cast<float4*>(oxy + 2 * sw) = xy01;
+        *reinterpret_cast<float4*>(oxy + 2 * (2 ^ sw)) = xy23;
+        *reinterpret_cast<float4*>(ovxy + 2 * sw) = vxy01;
+        *reinterpret_cast<float4*>(ovxy + 2 * (2 ^ sw)) = vxy23;
+        *reinterpret_cast<float4*>(oz) = z4;
+        *reinterpret_cast<float4*>(oz + S) = vz4;
+        if (PEER && (Rf < a.u0 + 2 || Rf >= a.u1 - 2))  // fused halo exchange, boundary rows
+#pragma unroll 1
+          for (int side = 0; side < 2; ++side) {
+            float* po = a.peer_out[side];
+            if (po == nullptr || (side == 0 ? Rf >= a.u0 + 2 : Rf < a.u1 - 2)) continue;
+            const int64_t S2 = a.peer_S[side];
+            const int64_t lr2 = Rf - a.peer_g0[side];
+            float* pb = po + static_cast<int64_t>(b) * 6 * S2;
+            float* pxy = pb + 2 * (lr2 * a.pitch + ix0);
+            float* pz = pb + 4 * S2 + lr2 * a.pitch + ix0;
+            *reinterpret_cast<float4*>(pxy + 2 * sw) = xy01;
+            *reinterpret_cast<float4*>(pxy + 2 * (2 ^ sw)) = xy23;
+            *reinterpret_cast<float4*>(pxy + 2 * S2 + 2 * sw) = vxy01;
+            *reinterpret_cast<float4*>(pxy + 2 * S2 + 2 * (2 ^ sw)) = vxy23;
+            *reinterpret_cast<float4*>(pz) = z4;
+            *reinterpret_cast<float4*>(pz + S2) = vz4;
+          }
+        if (a.constrained)
+          *reinterpret_cast<uchar4*>(a.constrained + b * nodes + static_cast<int64_t>(Rf) * nx +
+                                     ix0) = make_uchar4(mk[0], mk[1], mk[2], mk[3]);
       } else {
-        // colliders / pressure / mask: one node at a time (compact code, same IEEE-exact chain)
+        // pressure plug: one node at a time (compact code, same IEEE-exact chain)
         const float* rs = ring + s3 * ROWF;  // row Rf-1
 #pragma unroll
         for (int k = 0; k < 4; ++k) {

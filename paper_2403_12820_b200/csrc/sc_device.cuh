@@ -180,85 +180,83 @@ __device__ __forceinline__ void plug_tail(const ClothConst<T>& cc, const T v[3],
   }
 }
 
+// The collider responses of advance_with_impulse, one collider and one node per call, so the
+// FAST collider finish can run them collider-outer / node-inner with the same per-node sequence.
 template <typename T>
-__device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothConst<T>& cc,
-                                             int row, int64_t gnode, const T x[3], const T v[3],
-                                             const T imp[3], T xo[3], T vo[3], uint8_t& mask) {
+__device__ __forceinline__ void sphere_velocity(const SphereConst<T>& sp, const T x[3], T vv[3],
+                                                uint8_t& mask) {  // kernels.hpp:213-225
   using R = RN<T>;
-  mask = 0;
-  T vv[3];
+  T r[3];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) vv[d] = R::add(v[d], imp[d]);
-  // velocity-level response on the OLD positions (kernels.hpp:213-225)
-  for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<T> sp = a.spheres[cc.sphere0 + s];
-    T r[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) r[d] = R::sub(x[d], sp.c[d]);
-    const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
-    if (dist > T(0) && dist <= sp.Rband) {
-      const T vn = R::div(R::add(R::add(R::mul(vv[0], r[0]), R::mul(vv[1], r[1])), R::mul(vv[2], r[2])), dist);
-      if (vn < T(0)) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const T nrm = R::div(r[d], dist);
-          vv[d] = R::mul(R::sub(vv[d], R::mul(nrm, vn)), sp.omf);
-        }
-        mask = 1;
-      }
-    }
-  }
-  for (int q = 0; q < cc.n_planes; ++q) {
-    const PlaneConst<T> pl = a.planes[cc.plane0 + q];
-    if (R::sub(x[2], pl.h) <= pl.band && vv[2] < T(0)) {
-      const T vn = vv[2];
-      vv[0] = R::mul(vv[0], pl.omf);
-      vv[1] = R::mul(vv[1], pl.omf);
-      vv[2] = R::mul(R::sub(vv[2], vn), pl.omf);
-      mask = 1;
-    }
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    vo[d] = vv[d];
-    xo[d] = R::add(x[d], R::mul(vv[d], cc.dt));
-  }
-  // position-level intersection elimination (kernels.hpp:229-244)
-  for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<T> sp = a.spheres[cc.sphere0 + s];
-    T r[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) r[d] = R::sub(xo[d], sp.c[d]);
-    const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
-    if (dist > T(0) && dist < sp.R) {
-      T nrm[3];
+  for (int d = 0; d < 3; ++d) r[d] = R::sub(x[d], sp.c[d]);
+  const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
+  if (dist > T(0) && dist <= sp.Rband) {
+    const T vn = R::div(R::add(R::add(R::mul(vv[0], r[0]), R::mul(vv[1], r[1])), R::mul(vv[2], r[2])), dist);
+    if (vn < T(0)) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        nrm[d] = R::div(r[d], dist);
-        xo[d] = R::add(sp.c[d], R::mul(nrm[d], sp.R));
+        const T nrm = R::div(r[d], dist);
+        vv[d] = R::mul(R::sub(vv[d], R::mul(nrm, vn)), sp.omf);
       }
-      const T vn = R::add(R::add(R::mul(vo[0], nrm[0]), R::mul(vo[1], nrm[1])), R::mul(vo[2], nrm[2]));
-      if (vn < T(0)) {
+      mask = 1;
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void plane_velocity(const PlaneConst<T>& pl, const T x[3], T vv[3],
+                                               uint8_t& mask) {
+  using R = RN<T>;
+  if (R::sub(x[2], pl.h) <= pl.band && vv[2] < T(0)) {
+    const T vn = vv[2];
+    vv[0] = R::mul(vv[0], pl.omf);
+    vv[1] = R::mul(vv[1], pl.omf);
+    vv[2] = R::mul(R::sub(vv[2], vn), pl.omf);
+    mask = 1;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void sphere_position(const SphereConst<T>& sp, T xo[3], T vo[3],
+                                                uint8_t& mask) {  // kernels.hpp:229-244
+  using R = RN<T>;
+  T r[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) vo[d] = R::mul(R::sub(vo[d], R::mul(nrm[d], vn)), sp.omf);
-      }
-      mask = 1;
+  for (int d = 0; d < 3; ++d) r[d] = R::sub(xo[d], sp.c[d]);
+  const T dist = R::sqrt(R::add(R::add(R::mul(r[0], r[0]), R::mul(r[1], r[1])), R::mul(r[2], r[2])));
+  if (dist > T(0) && dist < sp.R) {
+    T nrm[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      nrm[d] = R::div(r[d], dist);
+      xo[d] = R::add(sp.c[d], R::mul(nrm[d], sp.R));
     }
-  }
-  for (int q = 0; q < cc.n_planes; ++q) {
-    const PlaneConst<T> pl = a.planes[cc.plane0 + q];
-    if (xo[2] < pl.h) {
-      xo[2] = pl.h;
-      const T vn = vo[2];
-      if (vn < T(0)) {
-        vo[0] = R::mul(vo[0], pl.omf);
-        vo[1] = R::mul(vo[1], pl.omf);
-        vo[2] = R::mul(R::sub(vo[2], vn), pl.omf);
-      }
-      mask = 1;
+    const T vn = R::add(R::add(R::mul(vo[0], nrm[0]), R::mul(vo[1], nrm[1])), R::mul(vo[2], nrm[2]));
+    if (vn < T(0)) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) vo[d] = R::mul(R::sub(vo[d], R::mul(nrm[d], vn)), sp.omf);
     }
+    mask = 1;
   }
-  // Dirichlet re-pin last (kernels.hpp:245-251): bitmap + rank prefix -> anchor slot
+}
+template <typename T>
+__device__ __forceinline__ void plane_position(const PlaneConst<T>& pl, T xo[3], T vo[3],
+                                               uint8_t& mask) {
+  using R = RN<T>;
+  if (xo[2] < pl.h) {
+    xo[2] = pl.h;
+    const T vn = vo[2];
+    if (vn < T(0)) {
+      vo[0] = R::mul(vo[0], pl.omf);
+      vo[1] = R::mul(vo[1], pl.omf);
+      vo[2] = R::mul(R::sub(vo[2], vn), pl.omf);
+    }
+    mask = 1;
+  }
+}
+// Dirichlet re-pin (kernels.hpp:245-251): bitmap + rank prefix -> anchor slot
+template <typename T>
+__device__ __forceinline__ void repin(const StepArgs<T>& a, const ClothConst<T>& cc, int row,
+                                      int64_t gnode, T xo[3], T vo[3], uint8_t& mask) {
+  using R = RN<T>;
   if (cc.n_pins > 0 && row >= cc.pin_row_lo && row <= cc.pin_row_hi) {
     const int64_t w = cc.pin_word0 + (gnode >> 5);
     const uint32_t bits = __ldg(a.pin_bits + w);
@@ -274,6 +272,29 @@ __device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothCo
       mask = 1;
     }
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void advance_node(const StepArgs<T>& a, const ClothConst<T>& cc,
+                                             int row, int64_t gnode, const T x[3], const T v[3],
+                                             const T imp[3], T xo[3], T vo[3], uint8_t& mask) {
+  using R = RN<T>;
+  mask = 0;
+  T vv[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) vv[d] = R::add(v[d], imp[d]);
+  // velocity-level response on the OLD positions (kernels.hpp:213-225)
+  for (int s = 0; s < cc.n_spheres; ++s) sphere_velocity(a.spheres[cc.sphere0 + s], x, vv, mask);
+  for (int q = 0; q < cc.n_planes; ++q) plane_velocity(a.planes[cc.plane0 + q], x, vv, mask);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    vo[d] = vv[d];
+    xo[d] = R::add(x[d], R::mul(vv[d], cc.dt));
+  }
+  // position-level intersection elimination (kernels.hpp:229-244)
+  for (int s = 0; s < cc.n_spheres; ++s) sphere_position(a.spheres[cc.sphere0 + s], xo, vo, mask);
+  for (int q = 0; q < cc.n_planes; ++q) plane_position(a.planes[cc.plane0 + q], xo, vo, mask);
+  repin(a, cc, row, gnode, xo, vo, mask);  // Dirichlet re-pin last
 }
 
 // ---- pressure plug (accumulate_pressure kernels.hpp:142-155 + scaling :183-187) -----------
