@@ -891,8 +891,8 @@ __global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __gri
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
                                                       const int n_segs) {
-  // dynamic smem: [RING][ROWF] ring, then (only when some cloth needs the collider / pressure /
-  // mask finish) a [32][13] per-lane impulse scratch
+  // dynamic smem: [RING][ROWF] ring, then (RING = 5: some cloth plugs pressure) a [32][13]
+  // per-lane impulse scratch for the pressure finish
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[RING];
   float (*scratch)[13] = reinterpret_cast<float (*)[13]>(ring + RING * ROWF);
@@ -1058,7 +1058,10 @@ void* pick_multi(bool alpha1, int ring) {
 size_t fast_smem_bytes(int ring, bool general) {
   size_t pad = 0;
   if (const char* env = std::getenv("SC_FAST_SMEM_PAD")) pad = std::strtoul(env, nullptr, 10);
-  return sizeof(float) * (ring * ROWF + (general ? 32 * 13 : 0)) + pad;  // pad: tuning knob
+  // the per-lane impulse scratch serves only the pressure finish (RING = 5); the collider / mask
+  // finish keeps everything in registers, so `general` alone costs no shared memory
+  (void)general;
+  return sizeof(float) * (ring * ROWF + (ring == 5 ? 32 * 13 : 0)) + pad;  // pad: tuning knob
 }
 
 FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general) {

@@ -39,7 +39,7 @@ struct FastPlan {
   int64_t units;  // one single-warp CTA per (cloth, 128-column strip, row segment)
   size_t smem;
   int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
-  bool general;   // collider / pressure / mask finish compiled in (needs per-lane scratch)
+  bool general;   // some cloth takes the collider / pressure / mask finish
   int occupancy;  // resident CTAs per SM
   bool multi_ok;  // all units fit co-resident: the persistent multi-step kernel may run
   int multi_segs; // segments per strip column of the persistent kernel (co-resident units)
