@@ -1081,19 +1081,25 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   if (occ < 1) occ = 1;
   const int64_t slots = static_cast<int64_t>(sms) * occ;
   const int64_t columns = static_cast<int64_t>(batch) * p.n_strips;
-  // choose the number of row segments maximising wave efficiency, discounting the ~0.6-row
-  // tail each segment pays, with segments of at least 8 rows
+  // choose the number of row segments maximising  fill x warm x balance:
+  //  fill    — units / (waves x resident slots);
+  //  warm    — seg / (seg + 1.5): each unit re-computes ~1.1 rows of edges below / above its
+  //            segment and waits for its first three rows (measured, tools/batch_sweep.py);
+  //  balance — 1 - 0.1 / waves: a single wave ends on its late warps (an SMSP issues oldest
+  //            first, so its warps finish in tiers), later waves refill freed slots;
+  // with segments of at least 4 rows (small problems: many short units beat few long ones).
   double best = -1.0;
   int best_segs = 1;
-  const int max_segs = std::max(1, rows / 8);
+  const int max_segs = std::max(1, rows / 4);
   for (int segs = 1; segs <= max_segs && segs <= 4096; ++segs) {
     // segments of floor/ceil(rows / segs) rows (decode_unit spreads the boundaries evenly)
     const double seg_rows = static_cast<double>(rows) / segs;
     const int64_t units = columns * segs;
     const int64_t waves = (units + slots - 1) / slots;
     const double fill = static_cast<double>(units) / static_cast<double>(waves * slots);
-    const double warm = seg_rows / (seg_rows + 0.6);
-    const double eff = fill * warm;
+    const double warm = seg_rows / (seg_rows + 1.5);
+    const double balance = 1.0 - 0.1 / static_cast<double>(waves);
+    const double eff = fill * warm * balance;
     if (eff > best + 1e-9) {
       best = eff;
       best_segs = segs;
