@@ -460,7 +460,9 @@ __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int 
 // One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
 // tensor maps and writing a.out. `phase` carries the ring barriers' parity bits across calls
 // (the persistent kernel runs many units / steps on the same ring).
-template <bool ALPHA1, int RING, bool PEER = false>
+// GEN = false: no cloth of the launch takes the collider / pressure / mask finish, which is
+// then compiled out (fewer live registers around the row loop)
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
                                          const StepArgs<float>& a, const FastNet& f, int b,
                                          int strip, int y0, int y1, float* ring, uint64_t* full,
@@ -567,7 +569,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
     const int Rf = R - 2;
     if (Rf >= y0 && Rf < y1 && lane_live) {
       const int64_t lr = Rf - a.g0;
-      if (simple) {
+      if (!GEN || simple) {
         float2 xs[4], vs[4];
         float xz[4], vz[4];
         win4(row2 + XY_X, lane, xs);
@@ -885,7 +887,7 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 #ifndef SC_FAST_MINB
 #define SC_FAST_MINB 16
 #endif
-template <bool ALPHA1, int RING, bool PEER = false>
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true>
 __global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
@@ -918,7 +920,7 @@ __global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __gri
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING, PEER>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
+    run_unit<ALPHA1, RING, PEER, GEN>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
                                  phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
@@ -941,11 +943,11 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // the stencil's 2-node reach — published completion of step k-1 (acquire/release flags in
 // global memory). That covers both the read-after-write (halo rows of step k-1) and the
 // write-after-read (neighbours done reading the buffer this step overwrites) hazards.
-template <bool ALPHA1, int RING>
+template <bool ALPHA1, int RING, bool GEN = true>
 #ifndef SC_MULTI_MINB
 #define SC_MULTI_MINB 12
 #endif
-__global__ void __launch_bounds__(32, SC_MULTI_MINB) fast_multi_kernel(
+__global__ void __launch_bounds__(32, GEN ? SC_MULTI_MINB : 16) fast_multi_kernel(
     const __grid_constant__ CUtensorMap txy0, const __grid_constant__ CUtensorMap tz0,
     const __grid_constant__ CUtensorMap txy1, const __grid_constant__ CUtensorMap tz1,
     const StepArgs<float> a0, const FastNet f, const int n_strips, const int seg_rows,
@@ -986,7 +988,7 @@ __global__ void __launch_bounds__(32, SC_MULTI_MINB) fast_multi_kernel(
     a.out = even ? a0.out : const_cast<float*>(a0.in);
     a.k = k;
     if (y0 < y1)
-      run_unit<ALPHA1, RING>(even ? &txy0 : &txy1, even ? &tz0 : &tz1, a, f, b, strip, y0, y1,
+      run_unit<ALPHA1, RING, false, GEN>(even ? &txy0 : &txy1, even ? &tz0 : &tz1, a, f, b, strip, y0, y1,
                              ring, full, scratch, phase);
     __syncwarp();  // orders every lane's stores before lane 0's (cumulative) release
     if (threadIdx.x == 0) {
@@ -1034,6 +1036,10 @@ template <bool ALPHA1, int RING>
 void* kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING>);
 }
+template <bool ALPHA1, int RING>
+void* simple_kernel_ptr() {
+  return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false>);
+}
 
 void* pick_kernel(bool alpha1, int ring) {
   if (ring == 5) return alpha1 ? kernel_ptr<true, 5>() : kernel_ptr<false, 5>();
@@ -1049,8 +1055,16 @@ template <bool ALPHA1, int RING>
 void* multi_ptr() {
   return reinterpret_cast<void*>(fast_multi_kernel<ALPHA1, RING>);
 }
+template <bool ALPHA1, int RING>
+void* multi_simple_ptr() {
+  return reinterpret_cast<void*>(fast_multi_kernel<ALPHA1, RING, false>);
+}
 
-void* pick_multi(bool alpha1, int ring) {
+void* pick_multi(bool alpha1, int ring, bool general = true) {
+  if (!general) {
+    if (ring == 5) return alpha1 ? multi_simple_ptr<true, 5>() : multi_simple_ptr<false, 5>();
+    return alpha1 ? multi_simple_ptr<true, 4>() : multi_simple_ptr<false, 4>();
+  }
   if (ring == 5) return alpha1 ? multi_ptr<true, 5>() : multi_ptr<false, 5>();
   return alpha1 ? multi_ptr<true, 4>() : multi_ptr<false, 4>();
 }
@@ -1073,7 +1087,10 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = fast_smem_bytes(p.ring, general);
   for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring), pick_multi(true, p.ring),
-                  pick_multi(false, p.ring),
+                  p.ring == 5 ? simple_kernel_ptr<true, 5>() : simple_kernel_ptr<true, 4>(),
+                  p.ring == 5 ? simple_kernel_ptr<false, 5>() : simple_kernel_ptr<false, 4>(),
+                  pick_multi(false, p.ring), pick_multi(true, p.ring, false),
+                  pick_multi(false, p.ring, false),
                   p.ring == 5 ? peer_kernel_ptr<true, 5>() : peer_kernel_ptr<true, 4>(),
                   p.ring == 5 ? peer_kernel_ptr<false, 5>() : peer_kernel_ptr<false, 4>()})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1116,7 +1133,8 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   p.smem = smem;
   p.occupancy = occ;
   int occ_multi = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_multi, pick_multi(true, p.ring), 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_multi, pick_multi(true, p.ring, general), 32,
+                                                smem);
   p.multi_ok = p.units <= static_cast<int64_t>(sms) * occ_multi;  // every unit co-resident
   if (!p.multi_ok && occ_multi > 0) {
     // the persistent kernel's own segmentation: one co-resident unit per slot
@@ -1151,6 +1169,13 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
   const bool peer = a.peer_out[0] != nullptr || a.peer_out[1] != nullptr;
 #define SC_FK(A, R, P) cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P>, txy, tz, a, f, ns, sr, ng)
+#define SC_FS(A, R) \
+  cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false>, txy, tz, a, f, ns, sr, ng)
+  if (!peer && !p.general && a.constrained == nullptr) {  // simple finish only
+    if (p.ring == 5) return f.alpha1 ? SC_FS(true, 5) : SC_FS(false, 5);
+    return f.alpha1 ? SC_FS(true, 4) : SC_FS(false, 4);
+  }
+#undef SC_FS
   if (peer) {  // fused halo exchange (strip contexts linked with sc_ctx_set_peer)
     if (p.ring == 5) return f.alpha1 ? SC_FK(true, 5, true) : SC_FK(false, 5, true);
     return f.alpha1 ? SC_FK(true, 4, true) : SC_FK(false, 4, true);
@@ -1182,18 +1207,16 @@ cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int ns = p.n_strips, sr = p.seg_rows, ng = p.multi_segs;
-  if (p.ring == 5) {
-    if (f.alpha1)
-      return cudaLaunchKernelEx(&cfg, fast_multi_kernel<true, 5>, tin[0], tin[1], tout[0],
-                                tout[1], a, f, ns, sr, ng, steps, done);
-    return cudaLaunchKernelEx(&cfg, fast_multi_kernel<false, 5>, tin[0], tin[1], tout[0], tout[1],
-                              a, f, ns, sr, ng, steps, done);
+#define SC_MK(A, R, G)                                                                      \
+  cudaLaunchKernelEx(&cfg, fast_multi_kernel<A, R, G>, tin[0], tin[1], tout[0], tout[1], a, f, \
+                     ns, sr, ng, steps, done)
+  if (!p.general && a.constrained == nullptr) {
+    if (p.ring == 5) return f.alpha1 ? SC_MK(true, 5, false) : SC_MK(false, 5, false);
+    return f.alpha1 ? SC_MK(true, 4, false) : SC_MK(false, 4, false);
   }
-  if (f.alpha1)
-    return cudaLaunchKernelEx(&cfg, fast_multi_kernel<true, 4>, tin[0], tin[1], tout[0], tout[1],
-                              a, f, ns, sr, ng, steps, done);
-  return cudaLaunchKernelEx(&cfg, fast_multi_kernel<false, 4>, tin[0], tin[1], tout[0], tout[1], a,
-                            f, ns, sr, ng, steps, done);
+  if (p.ring == 5) return f.alpha1 ? SC_MK(true, 5, true) : SC_MK(false, 5, true);
+  return f.alpha1 ? SC_MK(true, 4, true) : SC_MK(false, 4, true);
+#undef SC_MK
 }
 
 }  // namespace scb
