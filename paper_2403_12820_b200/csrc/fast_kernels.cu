@@ -103,6 +103,13 @@ __device__ __forceinline__ float2 vfma(float2 a, float w, float2 c) {
 }
 __device__ __forceinline__ float vfmav(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ float2 vfmav(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// edge masks as bit patterns (0 or ~0): a LOP3 on the ALU pipe instead of an FMUL by 0 / 1
+__device__ __forceinline__ float vand(float a, uint32_t k) {
+  return __uint_as_float(__float_as_uint(a) & k);
+}
+__device__ __forceinline__ float2 vand(float2 a, uint32_t k) {
+  return make_float2(vand(a.x, k), vand(a.y, k));
+}
 __device__ __forceinline__ float vsplat(float w) { return w; }
 __device__ __forceinline__ float2 vsplat2(float w) { return make_float2(w, w); }
 __device__ __forceinline__ float vq(float dx) { return fmaf(dx, dx, 1.0f); }
@@ -185,7 +192,7 @@ __device__ __forceinline__ void win4(const float* xyplane, int lane, float2* o) 
 template <bool ALPHA1, bool GENERAL, bool TAIL, typename V>
 __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, const float* vR,
                                           const float* x1p, const float* v1p, const float* x2p,
-                                          const float* v2p, int lane, float mL, float mRt,
+                                          const float* v2p, int lane, uint32_t mL, uint32_t mRt,
                                           float m1, float m2, V (&A0)[4], V (&A1)[4], V (&A2)[4],
                                           V bias) {
   // windows are loaded right before their edge groups (rows R, R-2, R-1 in that order) so the
@@ -210,7 +217,7 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     for (int e = 1; e < 5; ++e) {
       V dx = vsub(x1[e + 1], xr[e + 2]), dv = vsub(v1[e + 1], vr[e + 2]);
       if (e == 4) {
-        dx = vscale(dx, mRt);
+        dx = vand(dx, mRt);
       }
       edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[e - 1], dummy);
     }
@@ -218,7 +225,7 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
     for (int e = 0; e < 4; ++e) {
       V dx = vsub(x1[e + 2], xr[e + 1]), dv = vsub(v1[e + 2], vr[e + 1]);
       if (e == 0) {
-        dx = vscale(dx, mL);
+        dx = vand(dx, mL);
       }
       edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[e], dummy);
     }
@@ -233,8 +240,7 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   for (int e = 0; e < 5; ++e) {
     V dx = vsub(xr[e + 1], xr[e + 2]), dv = vsub(vr[e + 1], vr[e + 2]);
     if (e == 0 || e == 4) {
-      const float m = e == 0 ? mL : mRt;
-      dx = vscale(dx, m);
+      dx = vand(dx, e == 0 ? mL : mRt);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, A2[3], dummy);
@@ -245,8 +251,7 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   for (int e = 0; e < 6; ++e) {
     V dx = vsub(xr[e], xr[e + 2]), dv = vsub(vr[e], vr[e + 2]);
     if (e <= 1 || e >= 4) {
-      const float m = e <= 1 ? mL : mRt;
-      dx = vscale(dx, m);
+      dx = vand(dx, e <= 1 ? mL : mRt);
     }
     if (e <= 1) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy, A2[e]);
     else if (e >= 4) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[e - 2], dummy);
@@ -279,8 +284,8 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   for (int e = 0; e < 5; ++e) {
     V dx = vsub(x1[e + 1], xr[e + 2]), dv = vsub(v1[e + 1], vr[e + 2]);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
-      dx = vscale(dx, m);
+      if (e == 0 || e == 4) dx = vand(dx, e == 0 ? mL : mRt);
+      if (GENERAL) dx = vscale(dx, m1);
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, A2[0]);
     else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, A1[3], dummy);
@@ -291,8 +296,8 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   for (int e = 0; e < 5; ++e) {
     V dx = vsub(x1[e + 2], xr[e + 1]), dv = vsub(v1[e + 2], vr[e + 1]);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
-      dx = vscale(dx, m);
+      if (e == 0 || e == 4) dx = vand(dx, e == 0 ? mL : mRt);
+      if (GENERAL) dx = vscale(dx, m1);
     }
     if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, A1[0], dummy);
     else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, A2[3]);
@@ -324,7 +329,7 @@ __device__ __forceinline__ float zw(const float2* w, int i) { return (i & 1) ? w
 template <bool ALPHA1, bool GENERAL, bool TAIL>
 __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, const float* vR,
                                             const float* x1p, const float* v1p, const float* x2p,
-                                            const float* v2p, int lane, float mL, float mRt,
+                                            const float* v2p, int lane, uint32_t mL, uint32_t mRt,
                                             float m1, float m2, float2 (&A0)[2], float2 (&A1)[2],
                                             float2 (&A2)[2], float bias) {
   float2 xr[4], vr[4], x1[4], v1[4], x2[2], v2[2];
@@ -349,7 +354,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     for (int e = 1; e < 5; ++e) {
       float dx = zw(x1, e + 1) - zw(xr, e + 2), dv = zw(v1, e + 1) - zw(vr, e + 2);
       if (e == 4) {
-        dx *= mRt;
+        dx = vand(dx, mRt);
       }
       edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, e - 1), dummy);
     }
@@ -357,7 +362,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     for (int e = 0; e < 4; ++e) {
       float dx = zw(x1, e + 2) - zw(xr, e + 1), dv = zw(v1, e + 2) - zw(vr, e + 1);
       if (e == 0) {
-        dx *= mL;
+        dx = vand(dx, mL);
       }
       edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, e), dummy);
     }
@@ -371,10 +376,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
     float dx = zw(xr, e + 1) - zw(xr, e + 2), dv = zw(vr, e + 1) - zw(vr, e + 2);
-    if (e == 0 || e == 4) {
-      const float m = e == 0 ? mL : mRt;
-      dx *= m;
-    }
+    if (e == 0 || e == 4) dx = vand(dx, e == 0 ? mL : mRt);
     if (e == 0) edge<ALPHA1, false, true>(f, 0, 2, dx, dv, dummy, zc(A2, 0));
     else if (e == 4) edge<ALPHA1, true, false>(f, 0, 2, dx, dv, zc(A2, 3), dummy);
     else edge<ALPHA1, true, true>(f, 0, 2, dx, dv, zc(A2, e - 1), zc(A2, e));
@@ -384,8 +386,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
   for (int j = 0; j < 3; ++j) {
     float2 dx = vsub(xr[j], xr[j + 1]), dv = vsub(vr[j], vr[j + 1]);
     if (j == 0 || j == 2) {
-      const float m = j == 0 ? mL : mRt;
-      dx = vscale(dx, m);
+      dx = vand(dx, j == 0 ? mL : mRt);
     }
     if (j == 0) edge<ALPHA1, false, true>(f, 8, 10, dx, dv, dummy2, A2[0]);
     else if (j == 2) edge<ALPHA1, true, false>(f, 8, 10, dx, dv, A2[1], dummy2);
@@ -417,8 +418,8 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
   for (int e = 0; e < 5; ++e) {
     float dx = zw(x1, e + 1) - zw(xr, e + 2), dv = zw(v1, e + 1) - zw(vr, e + 2);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
-      dx *= m;
+      if (e == 0 || e == 4) dx = vand(dx, e == 0 ? mL : mRt);
+      if (GENERAL) dx *= m1;
     }
     if (e == 0) edge<ALPHA1, false, true>(f, 4, 6, dx, dv, dummy, zc(A2, 0));
     else if (e == 4) edge<ALPHA1, true, false>(f, 4, 6, dx, dv, zc(A1, 3), dummy);
@@ -429,8 +430,8 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
   for (int e = 0; e < 5; ++e) {
     float dx = zw(x1, e + 2) - zw(xr, e + 1), dv = zw(v1, e + 2) - zw(vr, e + 1);
     if (GENERAL || e == 0 || e == 4) {
-      const float m = (e == 0 ? mL : (e == 4 ? mRt : 1.0f)) * (GENERAL ? m1 : 1.0f);
-      dx *= m;
+      if (e == 0 || e == 4) dx = vand(dx, e == 0 ? mL : mRt);
+      if (GENERAL) dx *= m1;
     }
     if (e == 0) edge<ALPHA1, true, false>(f, 5, 7, dx, dv, zc(A1, 0), dummy);
     else if (e == 4) edge<ALPHA1, false, true>(f, 5, 7, dx, dv, dummy, zc(A2, 3));
@@ -440,7 +441,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
 
 template <bool ALPHA1, bool GENERAL, bool TAIL>
 __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, const float* row1,
-                                         const float* row2, int lane, float mL, float mRt,
+                                         const float* row2, int lane, uint32_t mL, uint32_t mRt,
                                          float m1, float m2, float2 (&P0)[4], float2 (&P1)[4],
                                          float2 (&P2)[4], float2 (&Z0)[2], float2 (&Z1)[2],
                                          float2 (&Z2)[2]) {
@@ -515,8 +516,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   wait_slot(1);
 
   // nx % 4 == 0 (fast_supported): only a strip's outermost lanes own edges leaving the grid
-  const float mL = ix0 >= 1 ? 1.0f : 0.0f;
-  const float mRt = ix0 + 4 < nx ? 1.0f : 0.0f;
+  const uint32_t mL = ix0 >= 1 ? 0xffffffffu : 0u;
+  const uint32_t mRt = ix0 + 4 < nx ? 0xffffffffu : 0u;
   const bool lane_live = ix0 < nx;
 
   const ClothConst<float> cc = a.cloths[b];
