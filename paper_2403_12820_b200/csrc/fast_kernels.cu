@@ -79,6 +79,14 @@ __device__ __forceinline__ void tma_load_4d(float* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// one lane of the (converged) warp, without reading %tid (no S2R in the row loop)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}" : "=r"(p));
+  return p != 0;
+}
+
 // rsqrt without the denormal fix-up rsqrtf() carries under -ftz=false: q = 1 + a dx^2 >= 1.
 __device__ __forceinline__ float rsqrt_q(float q) {
   float r;
@@ -478,6 +486,15 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   const int r_first = y0 - 2;
   const int r_last = y1 + 1;
 
+  // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
+  const ClothConst<float> cc = a.cloths[b];
+  const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
+                      a.constrained == nullptr;
+  const int64_t nodes = static_cast<int64_t>(nx) * ny;
+  const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
+  const float dv_eff[3] = {cc.fin[0], cc.fin[1], cc.fin[2]};  // plugged gravity impulse or 0
+  const float drag_eff = cc.fin[3];                            // plugged drag coefficient or 0
+
   // ring slot t % RING of row r_first + t is tracked incrementally (no modulo in the loop); the
   // TMA operands are formed outside the lane-0 branch so they stay warp-uniform
   const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full);
@@ -486,7 +503,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
     const uint32_t dst = ring_s + static_cast<uint32_t>(sl) * (ROWF * 4);
     const uint32_t bar = full_s + static_cast<uint32_t>(sl) * 8;
     const int crow = crow0 + t;
-    if (lane == 0) {
+    if (elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "n"(ROW_BYTES)
@@ -520,13 +537,6 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   const uint32_t mRt = ix0 + 4 < nx ? 0xffffffffu : 0u;
   const bool lane_live = ix0 < nx;
 
-  const ClothConst<float> cc = a.cloths[b];
-  const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
-                      a.constrained == nullptr;
-  const int64_t nodes = static_cast<int64_t>(nx) * ny;
-  const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
-  const float dv_eff[3] = {cc.fin[0], cc.fin[1], cc.fin[2]};  // plugged gravity impulse or 0
-  const float drag_eff = cc.fin[3];                            // plugged drag coefficient or 0
 
   // accumulators [column] for rows R-2 (P0/Z0), R-1 (P1/Z1), R (P2/Z2): P = (x,y), Z = z
   float2 P0[4], P1[4], P2[4];
