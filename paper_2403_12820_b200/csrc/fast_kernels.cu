@@ -898,8 +898,12 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 #ifndef SC_FAST_MINB
 #define SC_FAST_MINB 16
 #endif
-template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true>
-__global__ void __launch_bounds__(32, SC_FAST_MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
+// MINB: resident CTAs per SM the register allocation targets. 16 (128 registers) suits short
+// segments and single waves; 12 (~160 registers: more independent edges in flight) runs the row
+// loop ~5% faster and wins on tall columns processed in several waves of long segments
+// (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5).
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB>
+__global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
                                                       const int n_strips, const int seg_rows,
@@ -1051,6 +1055,11 @@ template <bool ALPHA1, int RING>
 void* simple_kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false>);
 }
+constexpr int kWideMinB = 12;
+template <bool ALPHA1, int RING>
+void* wide_kernel_ptr() {
+  return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false, kWideMinB>);
+}
 
 void* pick_kernel(bool alpha1, int ring) {
   if (ring == 5) return alpha1 ? kernel_ptr<true, 5>() : kernel_ptr<false, 5>();
@@ -1100,6 +1109,8 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring), pick_multi(true, p.ring),
                   p.ring == 5 ? simple_kernel_ptr<true, 5>() : simple_kernel_ptr<true, 4>(),
                   p.ring == 5 ? simple_kernel_ptr<false, 5>() : simple_kernel_ptr<false, 4>(),
+                  p.ring == 5 ? wide_kernel_ptr<true, 5>() : wide_kernel_ptr<true, 4>(),
+                  p.ring == 5 ? wide_kernel_ptr<false, 5>() : wide_kernel_ptr<false, 4>(),
                   pick_multi(false, p.ring), pick_multi(true, p.ring, false),
                   pick_multi(false, p.ring, false),
                   p.ring == 5 ? peer_kernel_ptr<true, 5>() : peer_kernel_ptr<true, 4>(),
@@ -1107,30 +1118,49 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
-  const int64_t slots = static_cast<int64_t>(sms) * occ;
   const int64_t columns = static_cast<int64_t>(batch) * p.n_strips;
+  const int max_segs = std::max(1, rows / 4);
   // choose the number of row segments maximising  fill x warm x balance:
   //  fill    — units / (waves x resident slots);
   //  warm    — seg / (seg + 1.5): each unit re-computes ~1.1 rows of edges below / above its
   //            segment and waits for its first three rows (measured, tools/batch_sweep.py);
-  //  balance — 1 - 0.1 / waves: a single wave ends on its late warps (an SMSP issues oldest
-  //            first, so its warps finish in tiers), later waves refill freed slots;
+  //  balance — 1 - 0.1 / waves: a single wave ends on its late warps (an SMSP issues its warp
+  //            slots in a fixed order, so its warps finish in tiers), later waves refill freed
+  //            slots;
   // with segments of at least 4 rows (small problems: many short units beat few long ones).
-  double best = -1.0;
-  int best_segs = 1;
-  const int max_segs = std::max(1, rows / 4);
-  for (int segs = 1; segs <= max_segs && segs <= 4096; ++segs) {
-    // segments of floor/ceil(rows / segs) rows (decode_unit spreads the boundaries evenly)
-    const double seg_rows = static_cast<double>(rows) / segs;
-    const int64_t units = columns * segs;
-    const int64_t waves = (units + slots - 1) / slots;
-    const double fill = static_cast<double>(units) / static_cast<double>(waves * slots);
-    const double warm = seg_rows / (seg_rows + 1.5);
-    const double balance = 1.0 - 0.1 / static_cast<double>(waves);
-    const double eff = fill * warm * balance;
-    if (eff > best + 1e-9) {
-      best = eff;
-      best_segs = segs;
+  auto segment = [&](int occupancy) {
+    const int64_t slots = static_cast<int64_t>(sms) * occupancy;
+    double best = -1.0;
+    int best_segs = 1;
+    for (int segs = 1; segs <= max_segs && segs <= 4096; ++segs) {
+      // segments of floor/ceil(rows / segs) rows (decode_unit spreads the boundaries evenly)
+      const double seg_rows = static_cast<double>(rows) / segs;
+      const int64_t units = columns * segs;
+      const int64_t waves = (units + slots - 1) / slots;
+      const double fill = static_cast<double>(units) / static_cast<double>(waves * slots);
+      const double warm = seg_rows / (seg_rows + 1.5);
+      const double balance = 1.0 - 0.1 / static_cast<double>(waves);
+      const double eff = fill * warm * balance;
+      if (eff > best + 1e-9) {
+        best = eff;
+        best_segs = segs;
+      }
+    }
+    return best_segs;
+  };
+  int best_segs = segment(occ);
+  // simple-finish launches whose segments come out tall take the 12-CTA, wide-register kernel
+  // (measured: config 4's 55-row segments gain 5%; config 2's 15-row single wave loses 1%)
+  p.wide = false;
+  if (!general) {
+    int occ_w = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ_w, p.ring == 5 ? wide_kernel_ptr<true, 5>() : wide_kernel_ptr<true, 4>(), 32, smem);
+    p.wide = occ_w > 0 && rows / best_segs >= 32;
+    if (const char* env = std::getenv("SC_FAST_WIDE")) p.wide = occ_w > 0 && std::atoi(env) != 0;
+    if (p.wide) {
+      occ = occ_w;
+      best_segs = segment(occ);
     }
   }
   p.seg_rows = (rows + best_segs - 1) / best_segs;
@@ -1182,6 +1212,13 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
 #define SC_FK(A, R, P) cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P>, txy, tz, a, f, ns, sr, ng)
 #define SC_FS(A, R) \
   cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false>, txy, tz, a, f, ns, sr, ng)
+#define SC_FW(A, R) \
+  cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false, kWideMinB>, txy, tz, a, f, ns, sr, ng)
+  if (!peer && !p.general && a.constrained == nullptr && p.wide) {
+    if (p.ring == 5) return f.alpha1 ? SC_FW(true, 5) : SC_FW(false, 5);
+    return f.alpha1 ? SC_FW(true, 4) : SC_FW(false, 4);
+  }
+#undef SC_FW
   if (!peer && !p.general && a.constrained == nullptr) {  // simple finish only
     if (p.ring == 5) return f.alpha1 ? SC_FS(true, 5) : SC_FS(false, 5);
     return f.alpha1 ? SC_FS(true, 4) : SC_FS(false, 4);

@@ -1,5 +1,10 @@
-# usage: bash tools/ab.sh "<cfgs>"  — A/B device time: ab/libA.so vs the in-tree library, alternated
+# usage: bash tools/ab.sh "<cfgs>" [libs...] — alternated device timing of library builds
+# (default: ab/libA.so vs the in-tree library)
+cfgs=$1; shift
+libs=${@:-ab/libA.so tree}
 for i in 1 2; do
-  echo "A:"; SC_B200_LIB=ab/libA.so python tools/sched_check.py $1
-  echo "B:"; python tools/sched_check.py $1
+  for l in $libs; do
+    echo "$l:"
+    if [ "$l" = tree ]; then python tools/sched_check.py $cfgs; else SC_B200_LIB=$l python tools/sched_check.py $cfgs; fi
+  done
 done
