@@ -899,9 +899,10 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 #define SC_FAST_MINB 16
 #endif
 // MINB: resident CTAs per SM the register allocation targets. 16 (128 registers) suits short
-// segments and single waves; 12 (~160 registers: more independent edges in flight) runs the row
-// loop ~5% faster and wins on tall columns processed in several waves of long segments
-// (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5).
+// segments and single waves; 10 (160 registers, 12 CTAs/SM: more independent edges in flight)
+// runs the row loop ~5% faster and wins on tall columns processed in several waves of long
+// segments (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5;
+// MINB 8 = 206 registers is slower again: 631 us).
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB>
 __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
@@ -1055,7 +1056,7 @@ template <bool ALPHA1, int RING>
 void* simple_kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false>);
 }
-constexpr int kWideMinB = 12;
+constexpr int kWideMinB = 10;
 template <bool ALPHA1, int RING>
 void* wide_kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false, kWideMinB>);

@@ -40,7 +40,7 @@ struct FastPlan {
   size_t smem;
   int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
   bool general;   // some cloth takes the collider / pressure / mask finish
-  bool wide;      // simple finish on the 12-CTA, wide-register kernel (tall segments)
+  bool wide;      // simple finish on the wide-register kernel (160 registers, tall segments)
   int occupancy;  // resident CTAs per SM
   bool multi_ok;  // all units fit co-resident: the persistent multi-step kernel may run
   int multi_segs; // segments per strip column of the persistent kernel (co-resident units)
