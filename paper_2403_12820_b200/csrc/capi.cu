@@ -107,6 +107,7 @@ struct sc_ctx {
   int u0 = 0, u1 = 0;                   // owned global rows
   int pitch = 0;
   int64_t plane_stride = 0;
+  bool zs = false;  // z planes in the z_col swizzle (sc_device.cuh): FAST general-finish contexts
   bool has_scene = false, has_params = false;
   // device memory
   void* state[2] = {nullptr, nullptr};
@@ -435,6 +436,7 @@ StepArgs<T> base_args(sc_ctx* c) {
   a.u0 = c->u0;
   a.u1 = c->u1;
   a.batch = c->batch;
+  a.zs = c->zs ? 1 : 0;
   a.cloths = static_cast<const ClothConst<T>*>(c->cloths);
   a.spheres = static_cast<const SphereConst<T>*>(c->spheres);
   a.planes = static_cast<const PlaneConst<T>*>(c->planes);
@@ -526,12 +528,12 @@ void upload_state(sc_ctx* c, const void* x, const void* v) {
   if (c->prec == SC_F32)
     e = launch_aos_to_planar<float>(reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
                                     static_cast<float*>(c->state[c->cur]), c->batch, c->nx,
-                                    c->rows_local, c->plane_stride, c->pitch, c->stream);
+                                    c->rows_local, c->plane_stride, c->pitch, c->zs, c->stream);
   else
     e = launch_aos_to_planar<double>(reinterpret_cast<double*>(dx),
                                      reinterpret_cast<double*>(dv),
                                      static_cast<double*>(c->state[c->cur]), c->batch, c->nx,
-                                     c->rows_local, c->plane_stride, c->pitch, c->stream);
+                                     c->rows_local, c->plane_stride, c->pitch, c->zs, c->stream);
   ck(e, "aos_to_planar");
   c->launches.fetch_add(1);
 }
@@ -546,12 +548,12 @@ void download_state(sc_ctx* c, int which, void* x, void* v, bool sync = true) {
     e = launch_planar_to_aos<float>(static_cast<const float*>(c->state[which]),
                                     reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
                                     c->batch, c->nx, c->rows_local, c->plane_stride, c->pitch,
-                                    c->stream);
+                                    c->zs, c->stream);
   else
     e = launch_planar_to_aos<double>(static_cast<const double*>(c->state[which]),
                                      reinterpret_cast<double*>(dx),
                                      reinterpret_cast<double*>(dv), c->batch, c->nx,
-                                     c->rows_local, c->plane_stride, c->pitch, c->stream);
+                                     c->rows_local, c->plane_stride, c->pitch, c->zs, c->stream);
   ck(e, "planar_to_aos");
   c->launches.fetch_add(1);
   if (x) ck(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H x");
@@ -612,12 +614,12 @@ void frames_impl(sc_ctx* c, const void* x0, const void* v0, int steps, int strid
       e = launch_planar_to_aos<float>(static_cast<const float*>(c->state[c->cur]),
                                       reinterpret_cast<float*>(dx), reinterpret_cast<float*>(dv),
                                       c->batch, c->nx, c->rows_local, c->plane_stride, c->pitch,
-                                      c->stream);
+                                      c->zs, c->stream);
     else
       e = launch_planar_to_aos<double>(static_cast<const double*>(c->state[c->cur]),
                                        reinterpret_cast<double*>(dx),
                                        reinterpret_cast<double*>(dv), c->batch, c->nx,
-                                       c->rows_local, c->plane_stride, c->pitch, c->stream);
+                                       c->rows_local, c->plane_stride, c->pitch, c->zs, c->stream);
     ck(e, "planar_to_aos");
     c->launches.fetch_add(1);
     unsigned char* hx = direct ? ux + bytes * f : stage + 2 * bytes * slot;
@@ -781,6 +783,10 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       c->any_pressure = c->any_pressure || pres;
       c->any_general = c->any_general || pres || d.n_spheres > 0 || d.n_planes > 0;
     }
+    // the z-plane swizzle pays on the general-finish FAST kernel only (sc_device.cuh z_col); the
+    // state is (re)initialised after set_scene, so the layout is fixed here
+    c->zs = c->prec == SC_F32 && c->any_general;
+    if (const char* env = std::getenv("SC_ZSWIZZLE")) c->zs = c->prec == SC_F32 && std::atoi(env);
     if (c->prec == SC_F32) {
       build_tmaps(c);
       c->plan = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure,
@@ -1155,8 +1161,11 @@ void halo_copy(sc_ctx* c, int side, void* dev, bool pack, cudaStream_t st) {
     const int g = grow + r;
     if (g < 0 || g >= c->ny) continue;
     const int64_t lr = g - c->g0;
-    const int64_t seg_off[4] = {elem_index(0, lr, 0, c->pitch, S), elem_index(3, lr, 0, c->pitch, S),
-                                elem_index(2, lr, 0, c->pitch, S), elem_index(5, lr, 0, c->pitch, S)};
+    // whole rows: the column swizzles permute within 4-column groups only
+    const int64_t seg_off[4] = {elem_index(0, lr, 0, c->pitch, S, false),
+                                elem_index(3, lr, 0, c->pitch, S, false),
+                                elem_index(2, lr, 0, c->pitch, S, false),
+                                elem_index(5, lr, 0, c->pitch, S, false)};
     const int64_t seg_len[4] = {2LL * c->pitch, 2LL * c->pitch, c->pitch, c->pitch};
     int64_t hoff = static_cast<int64_t>(r) * 6 * c->pitch;
     for (int q = 0; q < 4; ++q) {

@@ -167,11 +167,31 @@ __device__ __forceinline__ void edge(const FastNet& f, int ca, int cb, V dx, V d
 // (sc_device.cuh): box column j of a strip (x0 a multiple of 128, box from x0-4) sits at
 // position xsw(j); a lane's four 2-column pieces are at xsw(4 lane + 2 + 2q), q = 0..3.
 __device__ __forceinline__ int xsw(int j) { return j ^ (((j + 28) >> 3) & 2); }
-__device__ __forceinline__ void win8(const float* zplane, int lane, float* o) {
-  const float2 l = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
-  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
-  const float2 r = *reinterpret_cast<const float2*>(zplane + FW * lane + 8);
-  o[0] = l.x; o[1] = l.y; o[2] = m.x; o[3] = m.y; o[4] = m.z; o[5] = m.w; o[6] = r.x; o[7] = r.y;
+// z planes: with the z_col swizzle (ZS, sc_device.cuh) box column j (global x0 - 4 + j) sits at
+// zsw(j) and a lane reads its window as 8-byte pieces at zsw(4 lane + 2 + 2q), conflict-free per
+// half-warp; on the plain layout it reads its own group in one 16-byte load
+template <bool ZS>
+__device__ __forceinline__ int zsw(int j) {
+  return ZS ? j ^ (((j + 124) >> 4) & 2) : j;
+}
+template <bool ZS>
+__device__ __forceinline__ float2 zpiece(const float* zplane, int j) {
+  return *reinterpret_cast<const float2*>(zplane + zsw<ZS>(j));
+}
+// a lane's 4 z values in the stored order of its group (halves swapped when ZS and column bit 5)
+template <bool ZS>
+__device__ __forceinline__ float4 zgroup(int ix0, float a, float b, float c, float d) {
+  return (ZS && ((ix0 >> 5) & 1)) ? make_float4(c, d, a, b) : make_float4(a, b, c, d);
+}
+template <bool ZS>
+__device__ __forceinline__ void win4z(const float* zplane, int lane, float* o) {
+  if constexpr (ZS) {
+    const float2 a = zpiece<ZS>(zplane, FW * lane + 4), b = zpiece<ZS>(zplane, FW * lane + 6);
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+  } else {
+    const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+    o[0] = m.x; o[1] = m.y; o[2] = m.z; o[3] = m.w;
+  }
 }
 __device__ __forceinline__ void win8(const float* xyplane, int lane, float2* o) {
 #pragma unroll
@@ -180,10 +200,6 @@ __device__ __forceinline__ void win8(const float* xyplane, int lane, float2* o) 
     o[2 * q] = make_float2(m.x, m.y);
     o[2 * q + 1] = make_float2(m.z, m.w);
   }
-}
-__device__ __forceinline__ void win4(const float* zplane, int lane, float* o) {
-  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
-  o[0] = m.x; o[1] = m.y; o[2] = m.z; o[3] = m.w;
 }
 __device__ __forceinline__ void win4(const float* xyplane, int lane, float2* o) {
   const float4 a = *reinterpret_cast<const float4*>(xyplane + 2 * xsw(FW * lane + 4));
@@ -317,39 +333,51 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
 __device__ __forceinline__ float& zc(float2 (&a)[2], int k) { return (k & 1) ? a[k >> 1].y : a[k >> 1].x; }
 
 // z windows as register pairs: columns ix0-2 .. ix0+5 (w8) and ix0 .. ix0+3 (w4)
+template <bool ZS>
 __device__ __forceinline__ void win8p(const float* zplane, int lane, float2* o) {
-  o[0] = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
-  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
-  o[1] = make_float2(m.x, m.y);
-  o[2] = make_float2(m.z, m.w);
-  o[3] = *reinterpret_cast<const float2*>(zplane + FW * lane + 8);
+  if constexpr (ZS) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = zpiece<ZS>(zplane, FW * lane + 2 + 2 * q);
+  } else {
+    o[0] = *reinterpret_cast<const float2*>(zplane + FW * lane + 2);
+    const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+    o[1] = make_float2(m.x, m.y);
+    o[2] = make_float2(m.z, m.w);
+    o[3] = *reinterpret_cast<const float2*>(zplane + FW * lane + 8);
+  }
 }
+template <bool ZS>
 __device__ __forceinline__ void win4p(const float* zplane, int lane, float2* o) {
-  const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
-  o[0] = make_float2(m.x, m.y);
-  o[1] = make_float2(m.z, m.w);
+  if constexpr (ZS) {
+    o[0] = zpiece<ZS>(zplane, FW * lane + 4);
+    o[1] = zpiece<ZS>(zplane, FW * lane + 6);
+  } else {
+    const float4 m = *reinterpret_cast<const float4*>(zplane + FW * lane + 4);
+    o[0] = make_float2(m.x, m.y);
+    o[1] = make_float2(m.z, m.w);
+  }
 }
 __device__ __forceinline__ float zw(const float2* w, int i) { return (i & 1) ? w[i >> 1].y : w[i >> 1].x; }
 
 // comp_pass for z with adjacent columns packed where the edge geometry keeps register pairs
 // aligned: E2 edges (offset 2) and the vertical N / N2 edges run two columns per FFMA2 / MUFU
 // pair; E, NE, NW (odd offsets) stay scalar on the pair halves.
-template <bool ALPHA1, bool GENERAL, bool TAIL>
+template <bool ALPHA1, bool GENERAL, bool TAIL, bool ZS>
 __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, const float* vR,
                                             const float* x1p, const float* v1p, const float* x2p,
                                             const float* v2p, int lane, uint32_t mL, uint32_t mRt,
                                             float m1, float m2, float2 (&A0)[2], float2 (&A1)[2],
                                             float2 (&A2)[2], float bias) {
   float2 xr[4], vr[4], x1[4], v1[4], x2[2], v2[2];
-  win8p(xR, lane, xr);
-  win8p(vR, lane, vr);
+  win8p<ZS>(xR, lane, xr);
+  win8p<ZS>(vR, lane, vr);
   float dummy = 0.f;
   float2 dummy2{};
   if (TAIL) {
-    win8p(x1p, lane, x1);
-    win8p(v1p, lane, v1);
-    win4p(x2p, lane, x2);
-    win4p(v2p, lane, v2);
+    win8p<ZS>(x1p, lane, x1);
+    win8p<ZS>(v1p, lane, v1);
+    win4p<ZS>(x2p, lane, x2);
+    win4p<ZS>(v2p, lane, v2);
     // N / N2 a-sides (packed), NE / NW a-sides (scalar)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -401,8 +429,8 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     else edge<ALPHA1, true, true>(f, 8, 10, dx, dv, A2[0], A2[1]);
   }
   // N2 edges (R-2 -> R), then N edges (R-1 -> R), packed column pairs
-  win4p(x2p, lane, x2);
-  win4p(v2p, lane, v2);
+  win4p<ZS>(x2p, lane, x2);
+  win4p<ZS>(v2p, lane, v2);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     float2 dx2 = vsub(x2[j], xr[j + 1]), dv2 = vsub(v2[j], vr[j + 1]);
@@ -411,8 +439,8 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
     }
     edge<ALPHA1, true, true>(f, 9, 11, dx2, dv2, A0[j], A2[j]);
   }
-  win8p(x1p, lane, x1);
-  win8p(v1p, lane, v1);
+  win8p<ZS>(x1p, lane, x1);
+  win8p<ZS>(v1p, lane, v1);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     float2 dx = vsub(x1[j + 1], xr[j + 1]), dv = vsub(v1[j + 1], vr[j + 1]);
@@ -447,7 +475,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
   }
 }
 
-template <bool ALPHA1, bool GENERAL, bool TAIL>
+template <bool ALPHA1, bool GENERAL, bool TAIL, bool ZS>
 __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, const float* row1,
                                          const float* row2, int lane, uint32_t mL, uint32_t mRt,
                                          float m1, float m2, float2 (&P0)[4], float2 (&P1)[4],
@@ -456,14 +484,15 @@ __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, co
   comp_pass<ALPHA1, GENERAL, TAIL, float2>(f, rowR + XY_X, rowR + XY_V, row1 + XY_X, row1 + XY_V,
                                            row2 + XY_X, row2 + XY_V, lane, mL, mRt, m1, m2, P0,
                                            P1, P2, make_float2(f.b[0], f.b[1]));
-  comp_pass_z<ALPHA1, GENERAL, TAIL>(f, rowR + Z_X, rowR + Z_V, row1 + Z_X, row1 + Z_V,
+  comp_pass_z<ALPHA1, GENERAL, TAIL, ZS>(f, rowR + Z_X, rowR + Z_V, row1 + Z_X, row1 + Z_V,
                                      row2 + Z_X, row2 + Z_V, lane, mL, mRt, m1, m2, Z0, Z1, Z2,
                                      f.b[2]);
 }
 
 // component d of x (X = true) or v at box column j of a ring slot
+template <bool ZS>
 __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int j) {
-  return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * xsw(j) + d] : slot[(X ? Z_X : Z_V) + j];
+  return d < 2 ? slot[(X ? XY_X : XY_V) + 2 * xsw(j) + d] : slot[(X ? Z_X : Z_V) + zsw<ZS>(j)];
 }
 
 // One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
@@ -471,7 +500,7 @@ __device__ __forceinline__ float slot_val(const float* slot, bool X, int d, int 
 // (the persistent kernel runs many units / steps on the same ring).
 // GEN = false: no cloth of the launch takes the collider / pressure / mask finish, which is
 // then compiled out (fewer live registers around the row loop)
-template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true>
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
                                          const StepArgs<float>& a, const FastNet& f, int b,
                                          int strip, int y0, int y1, float* ring, uint64_t* full,
@@ -566,13 +595,13 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
     const float* row2 = ring + s2 * ROWF;
     if (R >= y1) {
       if (R < ny)
-        row_pass<ALPHA1, false, true>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2,
+        row_pass<ALPHA1, false, true, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2,
                                       Z0, Z1, Z2);
     } else if (R >= 2) {
-      row_pass<ALPHA1, false, false>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2, Z0,
+      row_pass<ALPHA1, false, false, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2, Z0,
                                      Z1, Z2);
     } else {
-      row_pass<ALPHA1, true, false>(f, rowR, row1, row2, lane, mL, mRt, R >= 1 ? 1.f : 0.f, 0.f,
+      row_pass<ALPHA1, true, false, ZS>(f, rowR, row1, row2, lane, mL, mRt, R >= 1 ? 1.f : 0.f, 0.f,
                                     P0, P1, P2, Z0, Z1, Z2);
     }
 
@@ -585,8 +614,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         float xz[4], vz[4];
         win4(row2 + XY_X, lane, xs);
         win4(row2 + XY_V, lane, vs);
-        win4(row2 + Z_X, lane, xz);
-        win4(row2 + Z_V, lane, vz);
+        win4z<ZS>(row2 + Z_X, lane, xz);
+        win4z<ZS>(row2 + Z_V, lane, vz);
         // add_plug_impulse gravity/drag + advance without colliders (no mask, no contact
         // decision depends on it): FMA-contracted and x,y packed — part of FAST mode's 1e-5 bar
         float xo[3][4], vo[3][4];
@@ -653,8 +682,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
             make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
         *reinterpret_cast<float4*>(ovxy + 2 * (2 ^ sw)) =
             make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
-        *reinterpret_cast<float4*>(oz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
-        *reinterpret_cast<float4*>(oz + S) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
+        *reinterpret_cast<float4*>(oz) = zgroup<ZS>(ix0, xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
+        *reinterpret_cast<float4*>(oz + S) = zgroup<ZS>(ix0, vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         // fused halo exchange: the two owned rows at a peer side also go into the neighbour's
         // ghost rows (its output buffer, remote over NVLink)
         if (PEER && (Rf < a.u0 + 2 || Rf >= a.u1 - 2))  // boundary rows only
@@ -677,8 +706,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
               make_float4(vo[0][0], vo[1][0], vo[0][1], vo[1][1]);
           *reinterpret_cast<float4*>(pxy + 2 * S2 + 2 * (2 ^ sw2)) =
               make_float4(vo[0][2], vo[1][2], vo[0][3], vo[1][3]);
-          *reinterpret_cast<float4*>(pz) = make_float4(xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
-          *reinterpret_cast<float4*>(pz + S2) = make_float4(vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
+          *reinterpret_cast<float4*>(pz) = zgroup<ZS>(ix0, xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
+          *reinterpret_cast<float4*>(pz + S2) = zgroup<ZS>(ix0, vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         }
       } else if (!cc.plug_pressure) {
         // colliders and/or the contact mask: the lane's 4 nodes together (collider outer, node
@@ -688,8 +717,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         float xz[4], vz[4];
         win4(row2 + XY_X, lane, xs);
         win4(row2 + XY_V, lane, vs);
-        win4(row2 + Z_X, lane, xz);
-        win4(row2 + Z_V, lane, vz);
+        win4z<ZS>(row2 + Z_X, lane, xz);
+        win4z<ZS>(row2 + Z_V, lane, vz);
         float x[4][3], vo[4][3], xo[4][3];
         uint8_t mk[4];
         bool fin_imp = true;
@@ -761,8 +790,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         const float4 xy23 = make_float4(xo[2][0], xo[2][1], xo[3][0], xo[3][1]);
         const float4 vxy01 = make_float4(vo[0][0], vo[0][1], vo[1][0], vo[1][1]);
         const float4 vxy23 = make_float4(vo[2][0], vo[2][1], vo[3][0], vo[3][1]);
-        const float4 z4 = make_float4(xo[0][2], xo[1][2], xo[2][2], xo[3][2]);
-        const float4 vz4 = make_float4(vo[0][2], vo[1][2], vo[2][2], vo[3][2]);
+        const float4 z4 = zgroup<ZS>(ix0, xo[0][2], xo[1][2], xo[2][2], xo[3][2]);
+        const float4 vz4 = zgroup<ZS>(ix0, vo[0][2], vo[1][2], vo[2][2], vo[3][2]);
         float* ovxy = oxy + 2 * S;
         *reinterpret_cast<float4*>(oxy + 2 * sw) = xy01;
         *reinterpret_cast<float4*>(oxy + 2 * (2 ^ sw)) = xy23;
@@ -807,8 +836,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           float px[3], pv[3], imp[3], po[3], qo[3];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            px[d] = slot_val(row2, true, d, j);
-            pv[d] = slot_val(row2, false, d, j);
+            px[d] = slot_val<ZS>(row2, true, d, j);
+            pv[d] = slot_val<ZS>(row2, false, d, j);
             imp[d] = scratch[lane][4 * d + k];
           }
           if (a.health && !(isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]))) {
@@ -821,10 +850,10 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
             float e[3], n[3], w[3], sv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              e[d] = __fsub_rn(px[d], slot_val(row2, true, d, j + 1));
-              n[d] = __fsub_rn(px[d], slot_val(row1, true, d, j));
-              w[d] = __fsub_rn(px[d], slot_val(row2, true, d, j - 1));
-              sv[d] = __fsub_rn(px[d], slot_val(rs, true, d, j));
+              e[d] = __fsub_rn(px[d], slot_val<ZS>(row2, true, d, j + 1));
+              n[d] = __fsub_rn(px[d], slot_val<ZS>(row1, true, d, j));
+              w[d] = __fsub_rn(px[d], slot_val<ZS>(row2, true, d, j - 1));
+              sv[d] = __fsub_rn(px[d], slot_val<ZS>(rs, true, d, j));
             }
             pressure_plug(cc, interior, e, n, w, sv, imp);
           }
@@ -833,8 +862,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           advance_node(a, cc, Rf, gnode, px, pv, imp, po, qo, mk);
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            out_b[elem_index(d, lr, ix, a.pitch, S)] = po[d];
-            out_b[elem_index(3 + d, lr, ix, a.pitch, S)] = qo[d];
+            out_b[elem_index(d, lr, ix, a.pitch, S, ZS)] = po[d];
+            out_b[elem_index(3 + d, lr, ix, a.pitch, S, ZS)] = qo[d];
           }
           for (int side = 0; PEER && side < 2; ++side) {  // fused halo exchange (simple path)
             float* pp = a.peer_out[side];
@@ -844,8 +873,8 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
             const int64_t lr2 = Rf - a.peer_g0[side];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              pb[elem_index(d, lr2, ix, a.pitch, S2)] = po[d];
-              pb[elem_index(3 + d, lr2, ix, a.pitch, S2)] = qo[d];
+              pb[elem_index(d, lr2, ix, a.pitch, S2, ZS)] = po[d];
+              pb[elem_index(3 + d, lr2, ix, a.pitch, S2, ZS)] = qo[d];
             }
           }
           if (a.constrained) a.constrained[b * nodes + gnode] = mk;
@@ -903,7 +932,8 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 // runs the row loop ~5% faster and wins on tall columns processed in several waves of long
 // segments (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5;
 // MINB 8 = 206 registers is slower again: 631 us).
-template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB>
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB,
+          bool ZS = false>
 __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
@@ -936,7 +966,7 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING, PEER, GEN>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
+    run_unit<ALPHA1, RING, PEER, GEN, ZS>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
                                  phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
@@ -959,7 +989,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // the stencil's 2-node reach — published completion of step k-1 (acquire/release flags in
 // global memory). That covers both the read-after-write (halo rows of step k-1) and the
 // write-after-read (neighbours done reading the buffer this step overwrites) hazards.
-template <bool ALPHA1, int RING, bool GEN = true>
+template <bool ALPHA1, int RING, bool GEN = true, bool ZS = false>
 #ifndef SC_MULTI_MINB
 #define SC_MULTI_MINB 12
 #endif
@@ -1004,7 +1034,7 @@ __global__ void __launch_bounds__(32, GEN ? SC_MULTI_MINB : 16) fast_multi_kerne
     a.out = even ? a0.out : const_cast<float*>(a0.in);
     a.k = k;
     if (y0 < y1)
-      run_unit<ALPHA1, RING, false, GEN>(even ? &txy0 : &txy1, even ? &tz0 : &tz1, a, f, b, strip, y0, y1,
+      run_unit<ALPHA1, RING, false, GEN, ZS>(even ? &txy0 : &txy1, even ? &tz0 : &tz1, a, f, b, strip, y0, y1,
                              ring, full, scratch, phase);
     __syncwarp();  // orders every lane's stores before lane 0's (cumulative) release
     if (threadIdx.x == 0) {
@@ -1057,6 +1087,15 @@ void* simple_kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false>);
 }
 constexpr int kWideMinB = 10;
+template <bool ALPHA1, int RING>
+void* zs_kernel_ptr(bool peer) {
+  return peer ? reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, true, true, SC_FAST_MINB, true>)
+              : reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, true, SC_FAST_MINB, true>);
+}
+template <bool ALPHA1, int RING>
+void* zs_multi_ptr() {
+  return reinterpret_cast<void*>(fast_multi_kernel<ALPHA1, RING, true, true>);
+}
 template <bool ALPHA1, int RING>
 void* wide_kernel_ptr() {
   return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, RING, false, false, kWideMinB>);
@@ -1111,6 +1150,12 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
                   p.ring == 5 ? simple_kernel_ptr<true, 5>() : simple_kernel_ptr<true, 4>(),
                   p.ring == 5 ? simple_kernel_ptr<false, 5>() : simple_kernel_ptr<false, 4>(),
                   p.ring == 5 ? wide_kernel_ptr<true, 5>() : wide_kernel_ptr<true, 4>(),
+                  p.ring == 5 ? zs_kernel_ptr<true, 5>(false) : zs_kernel_ptr<true, 4>(false),
+                  p.ring == 5 ? zs_kernel_ptr<false, 5>(false) : zs_kernel_ptr<false, 4>(false),
+                  p.ring == 5 ? zs_kernel_ptr<true, 5>(true) : zs_kernel_ptr<true, 4>(true),
+                  p.ring == 5 ? zs_kernel_ptr<false, 5>(true) : zs_kernel_ptr<false, 4>(true),
+                  p.ring == 5 ? zs_multi_ptr<true, 5>() : zs_multi_ptr<true, 4>(),
+                  p.ring == 5 ? zs_multi_ptr<false, 5>() : zs_multi_ptr<false, 4>(),
                   p.ring == 5 ? wide_kernel_ptr<false, 5>() : wide_kernel_ptr<false, 4>(),
                   pick_multi(false, p.ring), pick_multi(true, p.ring, false),
                   pick_multi(false, p.ring, false),
@@ -1210,17 +1255,21 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
   const CUtensorMap& tz = tmap[1];
   const int ns = p.n_strips, sr = p.seg_rows, ng = p.n_segs;
   const bool peer = a.peer_out[0] != nullptr || a.peer_out[1] != nullptr;
-#define SC_FK(A, R, P) cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P>, txy, tz, a, f, ns, sr, ng)
+#define SC_FK(A, R, P)                                                                     \
+  (a.zs ? cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P, true, SC_FAST_MINB, true>, txy, tz, a, \
+                             f, ns, sr, ng)                                                    \
+        : cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, P>, txy, tz, a, f, ns, sr, ng))
 #define SC_FS(A, R) \
   cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false>, txy, tz, a, f, ns, sr, ng)
 #define SC_FW(A, R) \
   cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false, kWideMinB>, txy, tz, a, f, ns, sr, ng)
-  if (!peer && !p.general && a.constrained == nullptr && p.wide) {
+  const bool simple = !peer && !p.general && a.constrained == nullptr && !a.zs;
+  if (simple && p.wide) {
     if (p.ring == 5) return f.alpha1 ? SC_FW(true, 5) : SC_FW(false, 5);
     return f.alpha1 ? SC_FW(true, 4) : SC_FW(false, 4);
   }
 #undef SC_FW
-  if (!peer && !p.general && a.constrained == nullptr) {  // simple finish only
+  if (simple) {  // simple finish only (plain z layout)
     if (p.ring == 5) return f.alpha1 ? SC_FS(true, 5) : SC_FS(false, 5);
     return f.alpha1 ? SC_FS(true, 4) : SC_FS(false, 4);
   }
@@ -1256,16 +1305,24 @@ cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int ns = p.n_strips, sr = p.seg_rows, ng = p.multi_segs;
+#define SC_MZ(A, R)                                                                         \
+  cudaLaunchKernelEx(&cfg, fast_multi_kernel<A, R, true, true>, tin[0], tin[1], tout[0], tout[1], \
+                     a, f, ns, sr, ng, steps, done)
 #define SC_MK(A, R, G)                                                                      \
   cudaLaunchKernelEx(&cfg, fast_multi_kernel<A, R, G>, tin[0], tin[1], tout[0], tout[1], a, f, \
                      ns, sr, ng, steps, done)
-  if (!p.general && a.constrained == nullptr) {
+  if (!p.general && a.constrained == nullptr && !a.zs) {
     if (p.ring == 5) return f.alpha1 ? SC_MK(true, 5, false) : SC_MK(false, 5, false);
     return f.alpha1 ? SC_MK(true, 4, false) : SC_MK(false, 4, false);
+  }
+  if (a.zs) {
+    if (p.ring == 5) return f.alpha1 ? SC_MZ(true, 5) : SC_MZ(false, 5);
+    return f.alpha1 ? SC_MZ(true, 4) : SC_MZ(false, 4);
   }
   if (p.ring == 5) return f.alpha1 ? SC_MK(true, 5, true) : SC_MK(false, 5, true);
   return f.alpha1 ? SC_MK(true, 4, true) : SC_MK(false, 4, true);
 #undef SC_MK
+#undef SC_MZ
 }
 
 }  // namespace scb

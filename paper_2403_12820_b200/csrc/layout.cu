@@ -8,7 +8,8 @@ namespace {
 
 template <typename T>
 __global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, T* __restrict__ out,
-                              int batch, int nx, int rows, int64_t plane_stride, int pitch) {
+                              int batch, int nx, int rows, int64_t plane_stride, int pitch,
+                              bool zs) {
   const int64_t per = static_cast<int64_t>(rows) * nx;
   const int64_t total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -20,15 +21,16 @@ __global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, 
     T* o = out + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      o[elem_index(d, r, c, pitch, plane_stride)] = x[3 * i + d];
-      o[elem_index(3 + d, r, c, pitch, plane_stride)] = v[3 * i + d];
+      o[elem_index(d, r, c, pitch, plane_stride, zs)] = x[3 * i + d];
+      o[elem_index(3 + d, r, c, pitch, plane_stride, zs)] = v[3 * i + d];
     }
   }
 }
 
 template <typename T>
 __global__ void planar_to_aos(const T* __restrict__ in, T* __restrict__ x, T* __restrict__ v,
-                              int batch, int nx, int rows, int64_t plane_stride, int pitch) {
+                              int batch, int nx, int rows, int64_t plane_stride, int pitch,
+                              bool zs) {
   const int64_t per = static_cast<int64_t>(rows) * nx;
   const int64_t total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -40,8 +42,8 @@ __global__ void planar_to_aos(const T* __restrict__ in, T* __restrict__ x, T* __
     const T* s = in + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      if (x) x[3 * i + d] = s[elem_index(d, r, c, pitch, plane_stride)];
-      if (v) v[3 * i + d] = s[elem_index(3 + d, r, c, pitch, plane_stride)];
+      if (x) x[3 * i + d] = s[elem_index(d, r, c, pitch, plane_stride, zs)];
+      if (v) v[3 * i + d] = s[elem_index(3 + d, r, c, pitch, plane_stride, zs)];
     }
   }
 }
@@ -56,29 +58,29 @@ int grid_for(int64_t total) {
 
 template <typename T>
 cudaError_t launch_aos_to_planar(const T* x, const T* v, T* planar, int batch, int nx, int rows,
-                                 int64_t plane_stride, int pitch, cudaStream_t stream) {
+                                 int64_t plane_stride, int pitch, bool zs, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(batch) * rows * nx;
   aos_to_planar<T><<<grid_for(total), 256, 0, stream>>>(x, v, planar, batch, nx, rows,
-                                                       plane_stride, pitch);
+                                                       plane_stride, pitch, zs);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_planar_to_aos(const T* planar, T* x, T* v, int batch, int nx, int rows,
-                                 int64_t plane_stride, int pitch, cudaStream_t stream) {
+                                 int64_t plane_stride, int pitch, bool zs, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(batch) * rows * nx;
   planar_to_aos<T><<<grid_for(total), 256, 0, stream>>>(planar, x, v, batch, nx, rows,
-                                                       plane_stride, pitch);
+                                                       plane_stride, pitch, zs);
   return cudaGetLastError();
 }
 
 template cudaError_t launch_aos_to_planar<float>(const float*, const float*, float*, int, int, int,
-                                                 int64_t, int, cudaStream_t);
+                                                 int64_t, int, bool, cudaStream_t);
 template cudaError_t launch_aos_to_planar<double>(const double*, const double*, double*, int, int,
-                                                  int, int64_t, int, cudaStream_t);
+                                                  int, int64_t, int, bool, cudaStream_t);
 template cudaError_t launch_planar_to_aos<float>(const float*, float*, float*, int, int, int,
-                                                 int64_t, int, cudaStream_t);
+                                                 int64_t, int, bool, cudaStream_t);
 template cudaError_t launch_planar_to_aos<double>(const double*, double*, double*, int, int, int,
-                                                  int64_t, int, cudaStream_t);
+                                                  int64_t, int, bool, cudaStream_t);
 
 }  // namespace scb

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
       const int lr = gy0 - 2 + ly - a.g0;
       T val = T(0);
       if (gx >= 0 && gx < a.nx && lr >= 0 && lr < rows_local)
-        val = in[elem_index(p, lr, gx, a.pitch, a.plane_stride)];
+        val = in[elem_index(p, lr, gx, a.pitch, a.plane_stride, a.zs)];
       sm[e] = val;
     }
     __syncthreads();
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
     const int64_t lr = iy - a.g0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      out[elem_index(d, lr, ix, a.pitch, a.plane_stride)] = xo[d];
-      out[elem_index(3 + d, lr, ix, a.pitch, a.plane_stride)] = vo[d];
+      out[elem_index(d, lr, ix, a.pitch, a.plane_stride, a.zs)] = xo[d];
+      out[elem_index(3 + d, lr, ix, a.pitch, a.plane_stride, a.zs)] = vo[d];
     }
     if (a.constrained) a.constrained[static_cast<int64_t>(b) * nodes + gnode] = mask;
     if (a.health && !(R::finite(xo[0]) && R::finite(xo[1]) && R::finite(xo[2]) &&

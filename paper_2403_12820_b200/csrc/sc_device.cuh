@@ -26,19 +26,28 @@ __host__ __device__ constexpr int off_dy(int c) {
        : c == 6 ? -1 : c == 7 ? -1 : c == 8 ? 0 : c == 9 ? 2 : c == 10 ? 0 : -2;
 }
 
-// Column swizzle of the interleaved (x, y) planes: within every aligned group of 4 columns whose
+// Column swizzles of the planes: within every aligned group of 4 columns whose
 // group index has bit 2 set (columns with bit 4 set), the two 2-column halves are swapped. A
 // FAST-kernel lane owns one group; with this layout the lanes of a quarter-warp read their
 // 16-byte window pieces from 8 distinct bank groups (the plain layout puts lanes l and l+4 on
 // the same banks). Pure permutation within a group: any row segment of whole groups is
 // contiguous, and every access goes through elem_index / xy_col.
 __host__ __device__ __forceinline__ int64_t xy_col(int64_t c) { return c ^ ((c >> 3) & 2); }
+// The same for the z planes with group-index bit 3 (columns with bit 5 set), in contexts whose
+// FAST launches take the general (collider / pressure / mask) finish (`zs`): a lane's 8-byte
+// window pieces (its own two halves and the neighbour halves of its halo) then come from 16
+// distinct bank pairs in every half-warp (the plain layout puts lanes l and l+8 on one pair).
+// Measured: config 5 (plane colliders) 696 -> 657 us/step; the simple-finish kernel is faster on
+// the plain layout (config 2: 45.9 vs 46.8 us), so collider-free contexts keep it.
+__host__ __device__ __forceinline__ int64_t z_col(int64_t c, bool zs) {
+  return zs ? c ^ ((c >> 4) & 2) : c;
+}
 
 // Element index of component p (0..5 = x.x x.y x.z v.x v.y v.z) of local row r, column c
 // within one cloth's block (see the layout above).
 __host__ __device__ __forceinline__ int64_t elem_index(int p, int64_t r, int64_t c, int64_t pitch,
-                                                       int64_t S) {
-  const int64_t rc = r * pitch + c;
+                                                       int64_t S, bool zs) {
+  const int64_t rc = r * pitch + z_col(c, zs);
   const int64_t rx = r * pitch + xy_col(c);
   switch (p) {
     case 0: return 2 * rx;
@@ -142,6 +151,7 @@ struct StepArgs {
   int32_t g0;            // global row of local row 0
   int32_t u0, u1;        // global rows to update [u0, u1)
   int32_t batch;
+  int32_t zs;            // z planes carry the z_col swizzle (contexts on the general finish)
   int32_t k;             // step index: t_next = T(k+1) * dt
   int32_t use_t_override;
   T t_override;

@@ -65,9 +65,10 @@ cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const 
 // (rows = the ctx's local rows; AoS arrays hold exactly those rows.)
 template <typename T>
 cudaError_t launch_aos_to_planar(const T* x_aos, const T* v_aos, T* planar, int batch, int nx,
-                                 int rows, int64_t plane_stride, int pitch, cudaStream_t stream);
+                                 int rows, int64_t plane_stride, int pitch, bool zs,
+                                 cudaStream_t stream);
 template <typename T>
 cudaError_t launch_planar_to_aos(const T* planar, T* x_aos, T* v_aos, int batch, int nx, int rows,
-                                 int64_t plane_stride, int pitch, cudaStream_t stream);
+                                 int64_t plane_stride, int pitch, bool zs, cudaStream_t stream);
 
 }  // namespace scb
