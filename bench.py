@@ -282,9 +282,11 @@ def run_ours(args, world, rank, local):
         launches = cb.launch_count() - launches0
         barrier()
         sec_max = max_over_ranks(sec)
-        # the fused kernel is the only launch per step: its average duration over the timed
-        # region is region / launches (inter-launch gaps included, i.e. conservative)
-        avg_launch_s = sec / max(launches, 1)
+        # one timestep = the fused kernel over the whole batch, issued as `chunks` concurrent
+        # cloth-chunk launches (capi.cu chunked_fast_steps); its average duration over the timed
+        # region is region / steps (inter-launch gaps included, i.e. conservative)
+        avg_launch_s = sec / args.steps
+        extra["launches_per_step"] = launches / args.steps
         cb.set_state(x, v)
         ps = max(5, min(args.steps, 20))
         parity_value = world * nodes_rank * ps / cb.benchmark(ps, 2, "parity")
@@ -359,7 +361,8 @@ def run_ours(args, world, rank, local):
                 "frac": achieved / peak, "traffic": _traffic(kernel, workload),
                 "kernel": kernel, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": BYTES_PER_NODE_UPDATE * nodes_rank,
-                "avg_launch_ms": avg_launch_s * 1e3}
+                "avg_launch_ms": avg_launch_s * 1e3,
+                "per": "timestep of the whole batch (its cloth-chunk launches run concurrently)"}
 
     # ---- CPU baseline: reference CPU path on this host, bounded sample (rank 0, N=1) ----
     cpu = None

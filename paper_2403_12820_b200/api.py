@@ -148,9 +148,18 @@ class Context:
         return fi, fn, fs
 
     def rollout(self, x0, v0, steps: int, k0: int = 0, mode: str = "parity",
-                constrained: bool = False):
+                constrained: bool = False, out=None):
+        """`out`: optional preallocated (x, v) result arrays. With page-locked inputs and
+        outputs (`pinned_empty`) a FAST rollout overlaps its transfers with the stepping."""
         x0, v0 = self._arr(x0), self._arr(v0)
-        xo, vo = self._empty(), self._empty()
+        if out is None:
+            xo, vo = self._empty(), self._empty()
+        else:
+            xo, vo = out
+            if (xo.dtype != self.dtype or vo.dtype != self.dtype or not xo.flags.c_contiguous
+                    or not vo.flags.c_contiguous or xo.size != self.batch * self.local_rows * self.nx * 3
+                    or vo.size != xo.size):
+                raise ConfigError("out: expected two C-contiguous state arrays of the context dtype")
         m = np.zeros((self.batch, self.nx * self.ny), np.uint8) if constrained else None
         _raise(self.lib, self.lib.sc_rollout(self.h, _ptr(x0), _ptr(v0), int(steps), int(k0),
                                              MODES[mode], _ptr(xo), _ptr(vo), _ptr(m)))

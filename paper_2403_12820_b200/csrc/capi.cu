@@ -156,6 +156,10 @@ struct sc_ctx {
   void* pin_stage = nullptr;
   size_t pin_stage_bytes = 0;
   cudaEvent_t frame_ev[2] = {nullptr, nullptr};
+  // pipelined host->host FAST rollout (sc_rollout): per-chunk streams and events
+  static constexpr int kPipe = 16;
+  cudaStream_t pipe_stream[kPipe] = {};
+  cudaEvent_t pipe_ev[kPipe + 1] = {};
 
   size_t elem() const { return prec == SC_F32 ? 4 : 8; }
   int64_t nodes_global() const { return static_cast<int64_t>(nx) * ny; }
@@ -634,6 +638,67 @@ void frames_impl(sc_ctx* c, const void* x0, const void* v0, int steps, int strid
   ck(cudaStreamSynchronize(c->stream), "sync");
 }
 
+// FAST stepping in cloth chunks on concurrent streams. Each chunk of cloths runs its own chain
+// of step launches (a slice of the whole-batch grid with the same plan: identical arithmetic,
+// bit-identical results), so one chunk's launch ramp and tail overlap the others' work instead
+// of leaving SMs idle at every step boundary (config 2: 46.0 -> ~42.6 us per step). `pre(i, q)`
+// and `post(i, q, buffer)` enqueue per-chunk work on chunk i's stream before its first and after
+// its last step (the pipelined rollout's transfers). Taken for FAST, f32, whole-cloth contexts
+// with >= 8 cloths and no mask output.
+int fast_chunks(const sc_ctx* c, int steps) {
+  int k = c->batch >= 16 ? 4 : 2;
+  if (const char* env = std::getenv("SC_CHUNKS")) k = std::min(sc_ctx::kPipe, std::atoi(env));
+  k = std::min(k, c->batch / 2);
+  if (k < 2 || c->prec != SC_F32 || !c->fast_ok || !c->tmap_ok || c->multi_on || c->peer_launch)
+    return 0;
+  if (c->u0 != 0 || c->u1 != c->ny || c->g0 != 0 || c->rows_local != c->ny) return 0;
+  if (c->batch < 8 || steps < 2) return 0;
+  return k;
+}
+
+template <typename Pre, typename Post>
+void chunked_fast_steps(sc_ctx* c, int K, int steps, int k0, Pre pre, Post post) {
+  for (int i = 0; i < K; ++i)
+    if (!c->pipe_stream[i])
+      ck(cudaStreamCreateWithFlags(&c->pipe_stream[i], cudaStreamNonBlocking), "stream");
+  for (cudaEvent_t& e : c->pipe_ev)
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  const FastPlan& full = c->plan;  // no mask: the launch-wide plan of this context
+  int b0[sc_ctx::kPipe + 1];
+  for (int i = 0; i <= K; ++i) b0[i] = static_cast<int>((static_cast<int64_t>(i) * c->batch) / K);
+  ck(cudaEventRecord(c->pipe_ev[K], c->stream), "event");  // earlier work on the ctx stream
+  for (int i = 0; i < K; ++i) {  // in chunk order (e.g. the uploads: one H2D copy engine)
+    ck(cudaStreamWaitEvent(c->pipe_stream[i], c->pipe_ev[K], 0), "wait");
+    pre(i, b0[i], b0[i + 1], c->pipe_stream[i]);
+  }
+  float* st[2] = {static_cast<float*>(c->state[c->cur]), static_cast<float*>(c->state[1 - c->cur])};
+  StepArgs<float> a = base_args<float>(c);
+  a.net = c->net32;
+  a.health = c->health_on ? c->health.p : nullptr;
+  for (int s = 0; s < steps; ++s) {  // step launches interleaved across the chunk streams
+    a.in = st[s & 1];
+    a.out = st[(s & 1) ^ 1];
+    a.k = k0 + s;
+    for (int i = 0; i < K; ++i) {
+      FastPlan p = full;
+      a.b_off = b0[i];
+      a.batch = b0[i + 1] - b0[i];
+      p.n_segs = p.chunk_segs;
+      p.seg_rows = (c->u1 - c->u0 + p.n_segs - 1) / p.n_segs;
+      p.units = static_cast<int64_t>(a.batch) * p.n_strips * p.n_segs;
+      ck(launch_fast(a, c->fast, c->tmap[c->cur ^ (s & 1)], p, c->pipe_stream[i]),
+         "kernel launch");
+    }
+  }
+  for (int i = 0; i < K; ++i) {
+    post(i, b0[i], b0[i + 1], c->pipe_stream[i], st[steps & 1]);
+    ck(cudaEventRecord(c->pipe_ev[i], c->pipe_stream[i]), "event");
+    ck(cudaStreamWaitEvent(c->stream, c->pipe_ev[i], 0), "wait");
+  }
+  c->launches.fetch_add(static_cast<int64_t>(K) * steps);
+  if (steps & 1) c->cur = 1 - c->cur;
+}
+
 void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last,
                   int kind = KIND_STEP) {
   if (steps < 0) throw_config("steps: must be >= 0");
@@ -660,6 +725,15 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
     if (multi & 1) c->cur = 1 - c->cur;
     s = multi;
   }
+  if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST) {
+    const int n = steps - (dev_mask_last ? 1 : 0);  // a mask-producing last step runs whole
+    const int K = fast_chunks(c, n);
+    if (K > 0) {
+      chunked_fast_steps(c, K, n, k0, [](int, int, int, cudaStream_t) {},
+                         [](int, int, int, cudaStream_t, const float*) {});
+      s = n;
+    }
+  }
   for (; s < steps; ++s) {
     const int k = k0 + s;
     uint8_t* m = (s == steps - 1) ? dev_mask_last : nullptr;
@@ -671,6 +745,58 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
                          c->health_on ? c->health.p : nullptr, c->u0, c->u1, c->stream);
     c->cur = 1 - c->cur;
   }
+}
+
+// Host -> host FAST rollout with the transfers overlapped: each chunk's H2D and layout conversion
+// precede its step chain on its stream, its conversion back and D2H follow it, so the copy
+// engines move chunk i while the SMs step the chunks already resident and the last chunks'
+// steps hide the first chunks' downloads. Needs page-locked host arrays.
+bool pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+bool rollout_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int k0, void* xo,
+                       void* vo) {
+  if (const char* env = std::getenv("SC_PIPELINE"))
+    if (std::atoi(env) == 0) return false;
+  const int K = fast_chunks(c, steps);
+  if (K == 0 || !xo || !vo) return false;
+  if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
+  const size_t cloth_bytes = static_cast<size_t>(c->nodes_local()) * 3 * sizeof(float);
+  const size_t bytes = cloth_bytes * c->batch;
+  c->aos.ensure(2 * bytes);
+  unsigned char* dx = c->aos.p;
+  unsigned char* dv = c->aos.p + bytes;
+  const int64_t S = c->plane_stride;
+  float* st0 = static_cast<float*>(c->state[c->cur]);
+  auto pre = [&](int, int b0, int b1, cudaStream_t q) {
+    const size_t off = cloth_bytes * b0, n = cloth_bytes * (b1 - b0);
+    ck(cudaMemcpyAsync(dx + off, static_cast<const unsigned char*>(x0) + off, n,
+                       cudaMemcpyHostToDevice, q), "H2D x");
+    ck(cudaMemcpyAsync(dv + off, static_cast<const unsigned char*>(v0) + off, n,
+                       cudaMemcpyHostToDevice, q), "H2D v");
+    ck(launch_aos_to_planar<float>(reinterpret_cast<float*>(dx + off),
+                                   reinterpret_cast<float*>(dv + off), st0 + b0 * 6 * S, b1 - b0,
+                                   c->nx, c->rows_local, S, c->pitch, c->zs, q), "aos_to_planar");
+  };
+  auto post = [&](int, int b0, int b1, cudaStream_t q, const float* fin) {
+    const size_t off = cloth_bytes * b0, n = cloth_bytes * (b1 - b0);
+    ck(launch_planar_to_aos<float>(fin + b0 * 6 * S, reinterpret_cast<float*>(dx + off),
+                                   reinterpret_cast<float*>(dv + off), b1 - b0, c->nx,
+                                   c->rows_local, S, c->pitch, c->zs, q), "planar_to_aos");
+    ck(cudaMemcpyAsync(static_cast<unsigned char*>(xo) + off, dx + off, n,
+                       cudaMemcpyDeviceToHost, q), "D2H x");
+    ck(cudaMemcpyAsync(static_cast<unsigned char*>(vo) + off, dv + off, n,
+                       cudaMemcpyDeviceToHost, q), "D2H v");
+  };
+  chunked_fast_steps(c, K, steps, k0, pre, post);
+  c->launches.fetch_add(2 * K);
+  return true;
 }
 
 }  // namespace
@@ -724,6 +850,10 @@ void sc_ctx_destroy(sc_ctx* c) {
       if (o) cudaIpcCloseMemHandle(o);
   c->peer_flags.release();
   if (c->pin_stage) cudaFreeHost(c->pin_stage);
+  for (cudaStream_t q : c->pipe_stream)
+    if (q) cudaStreamDestroy(q);
+  for (cudaEvent_t e : c->pipe_ev)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -885,6 +1015,11 @@ sc_status sc_rollout(sc_ctx* c, const void* x0, const void* v0, int32_t steps, i
     if (!x0 || !v0) throw_config("state: null array");
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_health(c);
+    if (!constrained && mode == SC_MODE_FAST && steps > 0 &&
+        rollout_pipelined(c, x0, v0, steps, k0, x_out, v_out)) {
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      return;
+    }
     upload_state(c, x0, v0);
     uint8_t* dm = nullptr;
     if (constrained && steps > 0) {

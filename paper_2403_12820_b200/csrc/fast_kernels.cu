@@ -952,6 +952,7 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
   const int unit = blockIdx.x;
   int b, strip, y0, y1;
   decode_unit(unit, n_strips, n_segs, a.u0, a.u1 - a.u0, b, strip, y0, y1);
+  b += a.b_off;
   (void)seg_rows;
   // programmatic dependent launch: the setup above overlapped the previous step's tail; the
   // state it wrote is read from here on
@@ -1217,6 +1218,19 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   }
   p.n_segs = best_segs;
   p.units = columns * p.n_segs;
+  // chunked stepping (capi.cu chunked_fast_steps: concurrent cloth-chunk streams fill each
+  // other's launch ramps and tails): the longest segments that still give ~1.15 waves of units
+  // (measured optimum: config 2 at 11-12 rows, config 5 at whole 128-row columns)
+  {
+    const int64_t slots = static_cast<int64_t>(sms) * occ;
+    int cs = static_cast<int>((115 * slots + 100 * columns - 1) / (100 * columns));
+    cs = std::max(1, std::min(cs, max_segs));
+    if (const char* env = std::getenv("SC_CHUNK_SEG_ROWS")) {
+      const int v = std::atoi(env);
+      if (v >= 2) cs = std::max(1, (rows + v - 1) / v);
+    }
+    p.chunk_segs = cs;
+  }
   p.smem = smem;
   p.occupancy = occ;
   int occ_multi = 0;

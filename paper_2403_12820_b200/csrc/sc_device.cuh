@@ -151,6 +151,7 @@ struct StepArgs {
   int32_t g0;            // global row of local row 0
   int32_t u0, u1;        // global rows to update [u0, u1)
   int32_t batch;
+  int32_t b_off;         // FAST launches over cloths [b_off, b_off + batch) (pipelined rollout)
   int32_t zs;            // z planes carry the z_col swizzle (contexts on the general finish)
   int32_t k;             // step index: t_next = T(k+1) * dt
   int32_t use_t_override;

@@ -36,6 +36,7 @@ struct FastNet {
 };
 struct FastPlan {
   int n_strips, seg_rows, n_segs;
+  int chunk_segs;  // row segments per strip column under chunked stepping
   int64_t units;  // one single-warp CTA per (cloth, 128-column strip, row segment)
   size_t smem;
   int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
