@@ -159,7 +159,9 @@ sc_status sc_ctx_set_persistent(sc_ctx* ctx, int32_t on);
 
 /* Host-to-host rollout: upload x0/v0, advance `steps`, download the final state. When
  * `constrained` is non-NULL it receives the mask of the LAST step ([batch][node] uint8, the
- * advance_with_impulse output of kernels.hpp:211-250). */
+ * advance_with_impulse output of kernels.hpp:211-250). FAST mode with >= 8 whole cloths, no mask
+ * and page-locked x0 / v0 / x_out / v_out (sc_host_alloc) overlaps the transfers with the stepping
+ * (cloth chunks on concurrent streams; results identical to the plain path). */
 sc_status sc_rollout(sc_ctx* ctx, const void* x0, const void* v0, int32_t steps, int32_t k0,
                      sc_mode mode, void* x_out, void* v_out, uint8_t* constrained);
 
