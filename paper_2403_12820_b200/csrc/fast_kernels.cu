@@ -213,7 +213,7 @@ __device__ __forceinline__ void win4(const float* xyplane, int lane, float2* o) 
 // mL / mRt zero the edges that leave the grid through a strip's boundary lane; GENERAL applies
 // the row masks of the first two rows of the cloth; TAIL (rows R >= y1, not owned) keeps only
 // the pushes into rows R-1 and R-2.
-template <bool ALPHA1, bool GENERAL, bool TAIL, typename V>
+template <bool ALPHA1, bool GENERAL, int TAIL, typename V>
 __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, const float* vR,
                                           const float* x1p, const float* v1p, const float* x2p,
                                           const float* v2p, int lane, uint32_t mL, uint32_t mRt,
@@ -222,9 +222,19 @@ __device__ __forceinline__ void comp_pass(const FastNet& f, const float* xR, con
   // windows are loaded right before their edge groups (rows R, R-2, R-1 in that order) so the
   // live register set stays small: R's window, then at most one of R-2 / R-1 beside it
   V xr[8], vr[8], x1[8], v1[8], x2[4], v2[4];
+  V dummy{};
+  if (TAIL == 2) {  // R = y1 + 1: row R-1 = y1 is not owned either, only N2 pushes into R-2
+    win4(xR, lane, xr);
+    win4(vR, lane, vr);
+    win4(x2p, lane, x2);
+    win4(v2p, lane, v2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      edge<ALPHA1, true, false>(f, 9, 11, vsub(x2[k], xr[k]), vsub(v2[k], vr[k]), A0[k], dummy);
+    return;
+  }
   win8(xR, lane, xr);
   win8(vR, lane, vr);
-  V dummy{};
   if (TAIL) {
     win8(x1p, lane, x1);
     win8(v1p, lane, v1);
@@ -362,17 +372,27 @@ __device__ __forceinline__ float zw(const float2* w, int i) { return (i & 1) ? w
 // comp_pass for z with adjacent columns packed where the edge geometry keeps register pairs
 // aligned: E2 edges (offset 2) and the vertical N / N2 edges run two columns per FFMA2 / MUFU
 // pair; E, NE, NW (odd offsets) stay scalar on the pair halves.
-template <bool ALPHA1, bool GENERAL, bool TAIL, bool ZS>
+template <bool ALPHA1, bool GENERAL, int TAIL, bool ZS>
 __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, const float* vR,
                                             const float* x1p, const float* v1p, const float* x2p,
                                             const float* v2p, int lane, uint32_t mL, uint32_t mRt,
                                             float m1, float m2, float2 (&A0)[2], float2 (&A1)[2],
                                             float2 (&A2)[2], float bias) {
   float2 xr[4], vr[4], x1[4], v1[4], x2[2], v2[2];
-  win8p<ZS>(xR, lane, xr);
-  win8p<ZS>(vR, lane, vr);
   float dummy = 0.f;
   float2 dummy2{};
+  if (TAIL == 2) {  // N2 a-sides only (packed)
+    win4p<ZS>(xR, lane, xr);
+    win4p<ZS>(vR, lane, vr);
+    win4p<ZS>(x2p, lane, x2);
+    win4p<ZS>(v2p, lane, v2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      edge<ALPHA1, true, false>(f, 9, 11, vsub(x2[j], xr[j]), vsub(v2[j], vr[j]), A0[j], dummy2);
+    return;
+  }
+  win8p<ZS>(xR, lane, xr);
+  win8p<ZS>(vR, lane, vr);
   if (TAIL) {
     win8p<ZS>(x1p, lane, x1);
     win8p<ZS>(v1p, lane, v1);
@@ -475,7 +495,7 @@ __device__ __forceinline__ void comp_pass_z(const FastNet& f, const float* xR, c
   }
 }
 
-template <bool ALPHA1, bool GENERAL, bool TAIL, bool ZS>
+template <bool ALPHA1, bool GENERAL, int TAIL, bool ZS>
 __device__ __forceinline__ void row_pass(const FastNet& f, const float* rowR, const float* row1,
                                          const float* row2, int lane, uint32_t mL, uint32_t mRt,
                                          float m1, float m2, float2 (&P0)[4], float2 (&P1)[4],
@@ -594,14 +614,21 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
     const float* row1 = ring + s1 * ROWF;
     const float* row2 = ring + s2 * ROWF;
     if (R >= y1) {
-      if (R < ny)
-        row_pass<ALPHA1, false, true, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2,
-                                      Z0, Z1, Z2);
+      // the second tail row only feeds row y1 - 1 through N2 edges (simple-finish kernels; the
+      // general-finish kernel measured faster with the one tail body)
+      if (R < ny) {
+        if (!GEN && R > y1)
+          row_pass<ALPHA1, false, 2, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1,
+                                         P2, Z0, Z1, Z2);
+        else
+          row_pass<ALPHA1, false, 1, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1,
+                                         P2, Z0, Z1, Z2);
+      }
     } else if (R >= 2) {
-      row_pass<ALPHA1, false, false, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2, Z0,
+      row_pass<ALPHA1, false, 0, ZS>(f, rowR, row1, row2, lane, mL, mRt, 1.f, 1.f, P0, P1, P2, Z0,
                                      Z1, Z2);
     } else {
-      row_pass<ALPHA1, true, false, ZS>(f, rowR, row1, row2, lane, mL, mRt, R >= 1 ? 1.f : 0.f, 0.f,
+      row_pass<ALPHA1, true, 0, ZS>(f, rowR, row1, row2, lane, mL, mRt, R >= 1 ? 1.f : 0.f, 0.f,
                                     P0, P1, P2, Z0, Z1, Z2);
     }
 
