@@ -30,3 +30,47 @@ def test_pipelined_rollout_bit_identical(monkeypatch, cfg_id, n, batch, steps):
     assert bits_equal(xb, xa) and bits_equal(vb, va)
     assert bits_equal(xc, xa) and bits_equal(vc, va)
     assert lp >= 2 * steps  # the pipelined path ran (one launch per chunk and step)
+
+
+@pytest.mark.parametrize("cfg_id,n,batch", [(2, 128, 16), (5, 128, 12), (2, 256, 9)])
+def test_chunked_stepping_bit_identical_to_whole_batch(monkeypatch, cfg_id, n, batch):
+    """Device-resident FAST stepping in concurrent cloth chunks (capi.cu chunked_fast_steps)
+    against one whole-batch launch per step: bit-identical states."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=n)
+    out = {}
+    for k in ("0", "2", "4"):
+        monkeypatch.setenv("SC_CHUNKS", k)
+        with ClothBatch(scenes, p) as cb:
+            cb.set_state(x, v)
+            l0 = cb.launch_count()
+            cb.advance(11, 0, "fast")
+            out[k] = cb.get_state() + (cb.launch_count() - l0,)
+    x0, v0, n0 = out["0"]
+    assert n0 >= 11
+    for k in ("2", "4"):
+        xk, vk, nk = out[k]
+        assert nk == n0 + 11 * (min(int(k), batch // 2) - 1)  # K launches per step
+        assert bits_equal(xk, x0) and bits_equal(vk, v0)
+
+
+def test_chunked_stepping_vs_oracle(oracle):
+    """Two FAST steps of 8 config-2 cloths (chunked: 2 chunks) from the oracle's state after 3
+    steps, within the FAST tolerance of the oracle's next two steps."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    from test_gpu_parity import fast_close
+    n, batch = 256, 8
+    cfg, scenes, p, x, v = configs.build(2, batch=batch, n=n)
+    keep = []
+    cds = [s.cloth_desc(keep) for s in scenes]
+    xs, vs, _ = oracle.rollout(n, n, cds, p.to_c(), x, v, 3)
+    xo, vo, _ = oracle.rollout(n, n, cds, p.to_c(), xs, vs, 2, 3)
+    with ClothBatch(scenes, p) as cb:
+        cb.set_state(xs, vs)
+        l0 = cb.launch_count()
+        cb.advance(2, 3, "fast")
+        assert cb.launch_count() - l0 >= 4  # 2 chunks x 2 steps
+        xf, vf = cb.get_state()
+    okx, ex = fast_close(xf, xo, 2e-5)
+    okv, ev = fast_close(vf, vo, 2e-5)
+    assert okx and okv, "rel err x %.3g v %.3g" % (ex, ev)
