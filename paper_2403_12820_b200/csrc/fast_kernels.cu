@@ -964,7 +964,7 @@ template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = 
 __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
-                                                      const int n_strips, const int seg_rows,
+                                                      const int n_strips, const int /*seg_rows*/,
                                                       const int n_segs) {
   // dynamic smem: [RING][ROWF] ring, then (RING = 5: some cloth plugs pressure) a [32][13]
   // per-lane impulse scratch for the pressure finish
@@ -980,7 +980,6 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
   int b, strip, y0, y1;
   decode_unit(unit, n_strips, n_segs, a.u0, a.u1 - a.u0, b, strip, y0, y1);
   b += a.b_off;
-  (void)seg_rows;
   // programmatic dependent launch: the setup above overlapped the previous step's tail; the
   // state it wrote is read from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
