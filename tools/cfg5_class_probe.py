@@ -1,0 +1,18 @@
+"""Config 5 FAST step time with the mixed classes vs simple-only / plane-only cloth sets
+(estimates what grouping cloths by boundary class could buy; development aid)."""
+import sys
+
+sys.path.insert(0, ".")
+import paper_2403_12820_b200.configs as C  # noqa: E402
+from paper_2403_12820_b200 import ClothBatch  # noqa: E402
+
+base = C.cloth_kind
+for label, fn in [("mixed", base), ("simple-only", lambda cfg, b: ("top_row", "corners")[b % 2]),
+                  ("plane-only", lambda cfg, b: "free")]:
+    C.cloth_kind = fn
+    cfg, scenes, p, x, v = C.build(5)
+    with ClothBatch(scenes, p) as cb:
+        cb.set_state(x, v)
+        sec = cb.benchmark(50, 3, "fast")
+    print(label, "%.1f us/step" % (sec / 50 * 1e6), flush=True)
+C.cloth_kind = base
