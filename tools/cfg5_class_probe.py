@@ -1,5 +1,7 @@
 """Config 5 FAST step time with the mixed classes vs simple-only / plane-only cloth sets
-(estimates what grouping cloths by boundary class could buy; development aid)."""
+(estimates what grouping cloths by boundary class could buy; development aid).
+SC_ZSWIZZLE=0/1 in the environment forces the z layout (1 on a collider-free set runs the
+general-finish kernel on it)."""
 import sys
 
 sys.path.insert(0, ".")
@@ -7,9 +9,10 @@ import paper_2403_12820_b200.configs as C  # noqa: E402
 from paper_2403_12820_b200 import ClothBatch  # noqa: E402
 
 base = C.cloth_kind
-for label, fn in [("mixed", base), ("simple-only", lambda cfg, b: ("top_row", "corners")[b % 2]),
-                  ("plane-only", lambda cfg, b: "free")]:
-    C.cloth_kind = fn
+sets = {"mixed": base, "simple-only": lambda cfg, b: ("top_row", "corners")[b % 2],
+        "plane-only": lambda cfg, b: "free"}
+for label in (sys.argv[1:] or list(sets)):
+    C.cloth_kind = sets[label]
     cfg, scenes, p, x, v = C.build(5)
     with ClothBatch(scenes, p) as cb:
         cb.set_state(x, v)
