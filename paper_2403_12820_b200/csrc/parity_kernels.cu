@@ -107,15 +107,18 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
       // total_impulse<T> (kernels.hpp:165-175): elastic, damping, pressure, external, * dt/m
       T f[3] = {T(0), T(0), T(0)};
       bool singular = false;
+      T lens[kChannels];  // |x_i - x_j| per channel: the damping loop reuses the elastic loop's
 #pragma unroll
       for (int c = 0; c < kChannels; ++c) {  // accumulate_elastic (kernels.hpp:86-108)
         const int jx = ix + off_dx(c), jy = iy + off_dy(c);
+        lens[c] = T(0);
         if (jx < 0 || jx >= a.nx || jy < 0 || jy >= a.ny) continue;
         T dd[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) dd[d] = R::sub(x[d], S(d, ly + off_dy(c), lx + off_dx(c)));
         const T len =
             R::sqrt(R::add(R::add(R::mul(dd[0], dd[0]), R::mul(dd[1], dd[1])), R::mul(dd[2], dd[2])));
+        lens[c] = len;
         if (len == T(0)) {
           singular = true;
           continue;
@@ -134,8 +137,7 @@ __global__ void __launch_bounds__(BX* BY) parity_kernel(const StepArgs<T> a) {
           dd[d] = R::sub(x[d], S(d, ly + off_dy(c), lx + off_dx(c)));
           dv[d] = R::sub(v[d], S(3 + d, ly + off_dy(c), lx + off_dx(c)));
         }
-        const T len =
-            R::sqrt(R::add(R::add(R::mul(dd[0], dd[0]), R::mul(dd[1], dd[1])), R::mul(dd[2], dd[2])));
+        const T len = lens[c];  // the same IEEE sqrt of the same operands (kernels.hpp:120-122)
         if (len == T(0)) continue;
         T dir[3];
 #pragma unroll
