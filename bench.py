@@ -103,6 +103,7 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_min_mhz": min(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": sorted(set().union(*[s[2] for s in self.samples])),
                 "samples": len(self.samples)}
