@@ -151,10 +151,12 @@ sc_status sc_ctx_get_health(sc_ctx* ctx, int32_t* first_bad_impulse_frame,
  * default for SC_F64 contexts (rollout's checks, eval.cpp:98-99, net.cpp:139-140), off for
  * SC_F32 (run_steps<float> checks nothing, eval.cpp:48-59). Per-operator calls always track. */
 sc_status sc_ctx_set_health_checks(sc_ctx* ctx, int32_t on);
-/* FAST mode runs multi-step advances as one persistent launch (units synchronise with their
- * stencil neighbours through global-memory step counters) when every unit fits co-resident;
- * off: one launch per step (programmatic dependent launch chains the steps). Default off: the
- * per-step path measured faster on B200 (neighbour polling costs more than launch gaps). */
+/* FAST mode runs multi-step advances of narrow-cloth batches (nx <= 128, no pressure plug) as
+ * one persistent wavefront launch: W timesteps per pass over HBM, rows updated in place in
+ * shared memory (wave_kernels.cu), bit-identical to one launch per step. Off: one streaming
+ * launch per step (programmatic dependent launch chains them). Default on; the environment
+ * variable SC_WAVE=0 turns it off for contexts that never called this. Mask-producing last steps
+ * and contexts outside the kernel's domain always take the streaming kernel. */
 sc_status sc_ctx_set_persistent(sc_ctx* ctx, int32_t on);
 
 /* Host-to-host rollout: upload x0/v0, advance `steps`, download the final state. When

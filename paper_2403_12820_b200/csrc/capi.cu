@@ -122,8 +122,6 @@ struct sc_ctx {
   DevBuf<Health> health;
   DevBuf<uint8_t> mask;
   DevBuf<unsigned char> aos;  // staging for AoS x, v, impulse
-  DevBuf<int32_t> done;       // per-unit step counters of the persistent FAST kernel
-  bool multi_on = false;      // persistent multi-step kernel (opt-in; per-step + PDL is faster)
   // params
   NetConst<float> net32{};
   NetConst<double> net64{};
@@ -131,6 +129,9 @@ struct sc_ctx {
   bool fast_ok = false;
   FastPlan plan{};       // simple finish (no colliders / pressure / mask)
   FastPlan plan_gen{};   // general finish
+  WavePlan wave{};       // wavefront temporal blocking (nx <= 128 batches, no pressure plug)
+  bool wave_on = true;   // sc_ctx_set_persistent / SC_WAVE=0: the streaming kernel only
+  bool wave_pinned = false;
   std::map<long long, FastPlan> plan_cache;  // row-range launches of strip contexts
   bool any_pressure = false, any_general = false;
   bool pbs_ok = false;  // every cloth has a grid spacing (rest lengths) for the PBS step
@@ -179,13 +180,23 @@ void free_scene(sc_ctx* c) {
   }
   c->pin_bits.release();
   c->pin_rank.release();
-  c->done.release();
   c->health.release();
   c->mask.release();
   c->aos.release();
   c->has_scene = false;
   c->tmap_ok = false;
   c->plan_cache.clear();
+  // a rebound scene must not keep pointers into the neighbours' (old) buffers
+  for (auto& q : c->peer) {
+    for (void*& o : q.opened)
+      if (o) {
+        cudaIpcCloseMemHandle(o);
+        o = nullptr;
+      }
+    q = sc_ctx::Peer{};
+  }
+  c->peer_count = 0;
+  c->peer_launch = false;
 }
 
 bool finite3(const double* v) {
@@ -645,11 +656,18 @@ void frames_impl(sc_ctx* c, const void* x0, const void* v0, int steps, int strid
 // and `post(i, q, buffer)` enqueue per-chunk work on chunk i's stream before its first and after
 // its last step (the pipelined rollout's transfers). Taken for FAST, f32, whole-cloth contexts
 // with >= 8 cloths and no mask output.
+// The wavefront kernel (wave_kernels.cu) applies: FAST f32 whole-cloth context, nx <= 128, no
+// pressure plug, not linked to strip peers, persistent stepping on (sc_ctx_set_persistent).
+bool wave_usable(const sc_ctx* c) {
+  return c->prec == SC_F32 && c->fast_ok && c->tmap_ok && c->wave.ok && c->wave_on &&
+         !c->peer_launch && c->strip_row0 < 0;
+}
+
 int fast_chunks(const sc_ctx* c, int steps) {
   int k = c->batch >= 16 ? 4 : 2;
   if (const char* env = std::getenv("SC_CHUNKS")) k = std::min(sc_ctx::kPipe, std::atoi(env));
   k = std::min(k, c->batch / 2);
-  if (k < 2 || c->prec != SC_F32 || !c->fast_ok || !c->tmap_ok || c->multi_on || c->peer_launch)
+  if (k < 2 || c->prec != SC_F32 || !c->fast_ok || !c->tmap_ok || c->peer_launch)
     return 0;
   if (c->u0 != 0 || c->u1 != c->ny || c->g0 != 0 || c->rows_local != c->ny) return 0;
   if (c->batch < 8 || steps < 2) return 0;
@@ -706,24 +724,19 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
   if (mode == SC_MODE_FAST && c->prec != SC_F32)
     throw_config("mode: FAST is an f32 mode (use PARITY with an f64 context)");
   int s = 0;
-  // FAST: the persistent multi-step kernel for all but a mask-producing last step
-  const int multi = (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok &&
-                     c->multi_on &&
-                     c->plan.multi_ok)
-                        ? steps - (dev_mask_last ? 1 : 0)
-                        : 0;
-  if (multi >= 2) {
-    StepArgs<float> a = base_args<float>(c);
-    a.k = k0;
-    a.net = c->net32;
-    a.health = c->health_on ? c->health.p : nullptr;
-    c->done.ensure(static_cast<size_t>(c->plan.n_strips) * c->batch * c->plan.multi_segs);
-    ck(launch_fast_multi(a, c->fast, c->tmap[c->cur], c->tmap[1 - c->cur], c->plan, multi,
-                         c->done.p, c->stream),
-       "kernel launch");
-    c->launches.fetch_add(2);  // counter init + persistent kernel
-    if (multi & 1) c->cur = 1 - c->cur;
-    s = multi;
+  if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST && wave_usable(c)) {
+    const int n = steps - (dev_mask_last ? 1 : 0);  // a mask-producing last step runs whole
+    if (n >= 2) {
+      StepArgs<float> a = base_args<float>(c);
+      a.out = static_cast<float*>(c->state[c->cur]);  // in place
+      a.k = k0;
+      a.net = c->net32;
+      a.health = c->health_on ? c->health.p : nullptr;
+      ck(launch_wave(a, c->fast, c->tmap[c->cur], c->wave, n, c->stream), "kernel launch");
+      c->launches.fetch_add(1);
+      k0 += n;  // the mask-producing last step (if any) follows below
+      steps -= n;
+    }
   }
   if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST) {
     const int n = steps - (dev_mask_last ? 1 : 0);  // a mask-producing last step runs whole
@@ -764,6 +777,7 @@ bool rollout_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int
                        void* vo) {
   if (const char* env = std::getenv("SC_PIPELINE"))
     if (std::atoi(env) == 0) return false;
+  if (wave_usable(c)) return false;  // one wavefront launch covers every cloth (TODO overlap)
   const int K = fast_chunks(c, steps);
   if (K == 0 || !xo || !vo) return false;
   if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
@@ -861,7 +875,8 @@ void sc_ctx_destroy(sc_ctx* c) {
 sc_status sc_ctx_set_strip(sc_ctx* c, int32_t row0, int32_t rows) {
   return guarded([&] {
     if (!c) throw_state("null context");
-    if (row0 < 0 || rows < 1) throw_config("strip: row0 must be >= 0 and rows >= 1");
+    // the stencil reaches 2 rows: a strip must own at least the 2 rows its halo ships
+    if (row0 < 0 || rows < 2) throw_config("strip: row0 must be >= 0 and rows >= 2");
     c->strip_row0 = row0;
     c->strip_rows = rows;
   });
@@ -922,9 +937,19 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       c->plan = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure,
                           c->any_general);
       c->plan_gen = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure, true);
+      c->wave = WavePlan{};
+      if (c->strip_row0 < 0 && !c->any_pressure)
+        c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general);
+      if (!c->wave_pinned) {
+        c->wave_on = true;
+        if (const char* env = std::getenv("SC_WAVE")) c->wave_on = std::atoi(env) != 0;
+      }
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
     c->has_scene = true;
+    // FAST eligibility depends on the grid (nx % 4) as well as the gains: re-derive it for
+    // the bound parameters whenever the scene changes
+    c->fast_ok = c->has_params && fast_supported(c->net32, c->nx);
   });
 }
 
@@ -936,7 +961,8 @@ sc_status sc_ctx_set_params(sc_ctx* c, const sc_params* p) {
     c->net32 = make_net<float>(p);
     c->net64 = make_net<double>(p);
     c->fast = make_fast_net(c->net32);
-    c->fast_ok = fast_supported(c->net32, c->nx);
+    // without a bound scene nx is unknown: sc_ctx_set_scene re-derives fast_ok
+    c->fast_ok = c->has_scene && fast_supported(c->net32, c->nx);
     c->has_params = true;
   });
 }
@@ -970,7 +996,8 @@ sc_status sc_ctx_advance(sc_ctx* c, int32_t steps, int32_t k0, sc_mode mode) {
 sc_status sc_ctx_set_persistent(sc_ctx* c, int32_t on) {
   return guarded([&] {
     if (!c) throw_state("null context");
-    c->multi_on = on != 0;
+    c->wave_on = on != 0;
+    c->wave_pinned = true;  // an explicit choice outlives later set_scene calls
   });
 }
 
@@ -1475,7 +1502,10 @@ sc_status sc_ctx_set_peer(sc_ctx* c, int32_t side, const sc_peer_export* nb, int
     // we are its neighbour on the opposite side
     q.flag = static_cast<unsigned*>(p[2]) + (side == 0 ? 1 : 0);
     c->peer_flags.ensure(2);
-    ck(cudaMemset(c->peer_flags.p, 0, 2 * sizeof(unsigned)), "memset");
+    // ordered on the ctx stream and complete before we return: the neighbours only signal
+    // after the caller's barrier that follows every set_peer, so no signal can be lost
+    ck(cudaMemsetAsync(c->peer_flags.p, 0, 2 * sizeof(unsigned), c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "sync");
     c->peer_count = 0;
   });
 }

@@ -14,14 +14,15 @@ namespace {
 constexpr int kThreads = 256;
 
 __global__ void frame_partials(const double* __restrict__ a, const double* __restrict__ b,
-                               int64_t nodes, int blocks_per_frame, double* __restrict__ partial) {
+                               int64_t nodes, int blocks_per_frame, int f0,
+                               double* __restrict__ partial) {
   __shared__ double sm[kThreads];
-  const int f = blockIdx.y;
+  const int64_t f = static_cast<int64_t>(f0) + blockIdx.y;
   const int64_t per_block = (nodes + blocks_per_frame - 1) / blocks_per_frame;
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * per_block;
   const int64_t i1 = i0 + per_block < nodes ? i0 + per_block : nodes;
-  const double* A = a + static_cast<int64_t>(f) * nodes * 3;
-  const double* B = b + static_cast<int64_t>(f) * nodes * 3;
+  const double* A = a + f * nodes * 3;
+  const double* B = b + f * nodes * 3;
   double acc = 0.0;
   for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
     const double dx = __dsub_rn(A[3 * i], B[3 * i]);
@@ -36,7 +37,7 @@ __global__ void frame_partials(const double* __restrict__ a, const double* __res
     if (threadIdx.x < s) sm[threadIdx.x] = __dadd_rn(sm[threadIdx.x], sm[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) partial[static_cast<int64_t>(f) * blocks_per_frame + blockIdx.x] = sm[0];
+  if (threadIdx.x == 0) partial[f * blocks_per_frame + blockIdx.x] = sm[0];
 }
 
 __global__ void frame_totals(const double* __restrict__ partial, int frames, int blocks_per_frame,
@@ -81,12 +82,26 @@ sc_status sc_evaluate_frames(int device, const double* test_x, const double* ref
       (e = cudaMallocAsync(&ds, sizeof(double) * frames, s)) != cudaSuccess) {
     st = fail("cudaMalloc", e);
   } else {
-    cudaMemcpyAsync(da, test_x, bytes, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(db, ref_x, bytes, cudaMemcpyHostToDevice, s);
-    frame_partials<<<dim3(bpf, frames), kThreads, 0, s>>>(da, db, nodes, bpf, dp);
-    frame_totals<<<(frames + 127) / 128, 128, 0, s>>>(dp, frames, bpf, ds);
-    cudaMemcpyAsync(frame_sums, ds, sizeof(double) * frames, cudaMemcpyDeviceToHost, s);
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) st = fail("evaluate", e);
+    if ((e = cudaMemcpyAsync(da, test_x, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(db, ref_x, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+      st = fail("H2D frames", e);
+    } else {
+      // gridDim.y is capped at 65535: frames go in chunks
+      for (int f0 = 0; f0 < frames && st == SC_OK; f0 += 65535) {
+        const int nf = frames - f0 < 65535 ? frames - f0 : 65535;
+        frame_partials<<<dim3(bpf, nf), kThreads, 0, s>>>(da, db, nodes, bpf, f0, dp);
+        if ((e = cudaGetLastError()) != cudaSuccess) st = fail("frame_partials launch", e);
+      }
+      if (st == SC_OK) {
+        frame_totals<<<(frames + 127) / 128, 128, 0, s>>>(dp, frames, bpf, ds);
+        if ((e = cudaGetLastError()) != cudaSuccess) st = fail("frame_totals launch", e);
+      }
+      if (st == SC_OK &&
+          (e = cudaMemcpyAsync(frame_sums, ds, sizeof(double) * frames, cudaMemcpyDeviceToHost,
+                               s)) != cudaSuccess)
+        st = fail("D2H sums", e);
+    }
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess && st == SC_OK) st = fail("evaluate", e);
   }
   cudaFreeAsync(da, s);
   cudaFreeAsync(db, s);

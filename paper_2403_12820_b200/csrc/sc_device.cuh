@@ -265,8 +265,8 @@ __device__ __forceinline__ void plane_position(const PlaneConst<T>& pl, T xo[3],
 }
 // Dirichlet re-pin (kernels.hpp:245-251): bitmap + rank prefix -> anchor slot
 template <typename T>
-__device__ __forceinline__ void repin(const StepArgs<T>& a, const ClothConst<T>& cc, int row,
-                                      int64_t gnode, T xo[3], T vo[3], uint8_t& mask) {
+__device__ __forceinline__ void repin_t(const StepArgs<T>& a, const ClothConst<T>& cc, int row,
+                                        int64_t gnode, T t_next, T xo[3], T vo[3], uint8_t& mask) {
   using R = RN<T>;
   if (cc.n_pins > 0 && row >= cc.pin_row_lo && row <= cc.pin_row_hi) {
     const int64_t w = cc.pin_word0 + (gnode >> 5);
@@ -274,7 +274,6 @@ __device__ __forceinline__ void repin(const StepArgs<T>& a, const ClothConst<T>&
     const uint32_t bit = 1u << (gnode & 31);
     if (bits & bit) {
       const int64_t slot = cc.anchor0 + __ldg(a.pin_rank + w) + __popc(bits & (bit - 1u));
-      const T t_next = a.use_t_override ? a.t_override : R::mul(T(a.k + 1), cc.dt);
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         vo[d] = cc.pin_u[d];
@@ -282,6 +281,15 @@ __device__ __forceinline__ void repin(const StepArgs<T>& a, const ClothConst<T>&
       }
       mask = 1;
     }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void repin(const StepArgs<T>& a, const ClothConst<T>& cc, int row,
+                                      int64_t gnode, T xo[3], T vo[3], uint8_t& mask) {
+  using R = RN<T>;
+  if (cc.n_pins > 0 && row >= cc.pin_row_lo && row <= cc.pin_row_hi) {
+    const T t_next = a.use_t_override ? a.t_override : R::mul(T(a.k + 1), cc.dt);
+    repin_t(a, cc, row, gnode, t_next, xo, vo, mask);
   }
 }
 

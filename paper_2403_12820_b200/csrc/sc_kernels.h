@@ -43,8 +43,6 @@ struct FastPlan {
   bool general;   // some cloth takes the collider / pressure / mask finish
   bool wide;      // simple finish on the wide-register kernel (160 registers, tall segments)
   int occupancy;  // resident CTAs per SM
-  bool multi_ok;  // all units fit co-resident: the persistent multi-step kernel may run
-  int multi_segs; // segments per strip column of the persistent kernel (co-resident units)
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
@@ -54,13 +52,26 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
 // tmap[1]: z planes, dims (pitch, rows, 2, batch) from element 4S, box (136,1,2,1).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
                         const FastPlan& plan, cudaStream_t stream);
-// `steps` FAST steps in one persistent launch (a.in -> a.out -> a.in ...); tin / tout: tensor
-// maps of a.in / a.out; done: per-unit step counters (plan.units ints).
 // debug: record [unit][start, end] globaltimer ns of every fast_step_kernel unit (nullptr: off)
 cudaError_t set_unit_timing(unsigned long long* dev_buf);
-cudaError_t launch_fast_multi(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tin,
-                              const CUtensorMap* tout, const FastPlan& plan, int steps, int* done,
-                              cudaStream_t stream);
+
+// wave_kernels.cu: wavefront temporal blocking of the FAST step for batches of narrow cloths
+// (nx <= 128): `levels` timesteps per pass over HBM, one persistent CTA per SM, state updated in
+// place (a.in == a.out), bit-identical to `levels` fast_step_kernel launches.
+struct WavePlan {
+  bool ok;        // the kernel applies to this grid / batch
+  int levels;     // W: timesteps per pass (= warps per CTA)
+  int slots;      // shared-memory ring slots (rows)
+  int ctas;       // persistent CTAs (one per SM, at most one per cloth)
+  size_t smem;
+  bool general;   // some cloth takes the collider finish
+};
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general);
+size_t wave_smem_bytes(int levels, int slots);
+// `steps` timesteps k = a.k .. a.k + steps - 1 of every cloth, in place in a.out (== a.in);
+// tmap: the tensor maps of that buffer.
+cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
+                        const WavePlan& plan, int steps, cudaStream_t stream);
 
 // layout.cu: AoS [batch][node][3] <-> planar [batch][6][rows][pitch]
 // (rows = the ctx's local rows; AoS arrays hold exactly those rows.)

@@ -1,0 +1,349 @@
+// Wavefront temporal blocking of the FAST step: several timesteps per HBM
+// round trip for batches of narrow cloths (nx <= 128: one 128-column strip per row).
+//
+// The reference advances every cloth one timestep per pass over memory (run_steps<T>,
+// eval.cpp:48-59: forward_impulse -> add_plug_impulse -> advance_with_impulse, kernels.hpp:
+// 179-282). The cell's reach is two rows (grid.cpp:14-30), and the FAST row pass finishes row
+// R-2 as soon as row R has been seen (fast_rowpass.cuh). So a row's new state can replace its
+// old state in place once the sweep is two rows past it, and a second sweep for the next
+// timestep can follow three rows behind the first, reading what the first one wrote. This kernel
+// runs W such sweeps at once:
+//
+//  * One persistent CTA per SM owns a contiguous range of cloths and W warps; warp w performs
+//    timestep w of every pass of W timesteps. Rows stream through a ring of shared-memory slots
+//    in a fixed order (pass-major, then cloth, then row, plus the two zero "tail" rows that
+//    separate consecutive cloths), so every warp walks the same sequence of slot positions.
+//  * Warp 0 also loads: TMA brings row positions a few steps ahead into their slots (rows past
+//    the cloth are zero-filled out of bounds, exactly like the streaming kernel's tails).
+//  * Warp w < W-1 writes the finished row back into its slot (level w+1) and arrives on the
+//    slot's level barrier; warp w+1 waits on it before its row pass. The last level stores the
+//    row to HBM (in place: the cloth's next pass reloads it later) and frees the slot for the
+//    loader. Every barrier is an mbarrier (hardware-suspended waits).
+//  * HBM traffic: 48 B per node per pass of W timesteps (48/W B per node-update). The arithmetic
+//    per step is the streaming kernel's row pass and finish called unchanged, so the results are
+//    bit-identical to W launches of fast_step_kernel.
+// Pressure plugs (whose finish reads the row below the finished one at the old level) and mask
+// output take the streaming kernel.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "fast_rowpass.cuh"
+#include "sc_device.cuh"
+#include "sc_kernels.h"
+
+namespace scb {
+
+namespace {
+
+using namespace fastrow;
+
+constexpr int kWavePrefetch = 4;  // row positions the loader runs ahead of warp 0
+
+// barriers addressed by 32-bit shared-window offsets computed once (no per-use address
+// conversion); waits ask the hardware to suspend the warp until the phase flips
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "n"(1000000)
+      : "memory");
+}
+
+// W warps, one CTA per SM. Dynamic smem: [slots][ROWF] ring, then the barriers
+// full[slots] (TMA landed), freeb[slots] (last level done with the slot),
+// lev[W-1][slots] (level w+1 of the slot's row written back).
+template <bool ALPHA1, int W, bool GEN, bool ZS>
+__global__ void __launch_bounds__(32 * W, 1)
+    wave_kernel(const __grid_constant__ CUtensorMap tmap_xy, const __grid_constant__ CUtensorMap tmap_z,
+                const StepArgs<float> a, const FastNet f, const int steps, const int slots) {
+  extern __shared__ __align__(128) float ring[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(slots) * ROWF);
+  uint64_t* freeb = full + slots;
+  uint64_t* lev = freeb + slots;
+  const int warp = static_cast<int>(threadIdx.x) >> 5;
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < slots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&freeb[s], 32);
+      for (int w = 0; w + 1 < W; ++w) mbar_init(&lev[w * slots + s], 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // this CTA's cloths [c0, c0 + m)
+  const int B = a.batch;
+  const int c0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * B / gridDim.x);
+  const int m = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * B / gridDim.x) - c0;
+  if (m <= 0) return;
+  const int nx = a.nx, ny = a.ny;
+  const int L = ny + 2;  // positions per (cloth, pass): rows 0..ny-1 and two zero tail rows
+  const int passes = (steps + W - 1) / W;
+  // position 0, 1: zero rows in front of the first cloth; then item i (pass i / m, cloth
+  // c0 + i % m) row R at position 2 + i L + R
+  const int Q = 2 + passes * m * L;
+
+  // ---- loader state (warp 0): its own cursor over (item, row) ----
+  int ld_q = 0, ld_R = ny, ld_c = c0, ld_ci = 0;  // positions 0, 1: rows ny, ny+1 (OOB: zeros)
+  int ld_s = 0;
+  uint64_t ph_free = 0;  // parity bits of freeb[] waits, per slot
+  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full), free_s = smem_u32(freeb);
+  const uint32_t lev_s = smem_u32(lev);
+  auto issue_next = [&]() {
+    if (ld_q >= Q) return;
+    if (ld_q >= slots) {  // the slot's previous row must be released by its last level
+      bar_wait(free_s + 8u * static_cast<uint32_t>(ld_s), static_cast<uint32_t>((ph_free >> ld_s) & 1u));
+      ph_free ^= 1ull << ld_s;
+    }
+    const uint32_t dst = ring_s + static_cast<uint32_t>(ld_s) * (ROWF * 4);
+    const uint32_t bar = full_s + static_cast<uint32_t>(ld_s) * 8;
+    const int crow = ld_R, cb = ld_c;
+    if (elect_one()) {
+      // the row was last written by generic stores (HBM: the previous pass's last level; smem:
+      // the levels of the slot's previous row): order them before the async-proxy copy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "n"(ROW_BYTES)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(&tmap_xy)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + Z_X * 4),
+          "l"(reinterpret_cast<uint64_t>(&tmap_z)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
+          : "memory");
+    }
+    // advance the cursor
+    ++ld_q;
+    ld_s = ld_s + 1 == slots ? 0 : ld_s + 1;
+    if (++ld_R == L) {
+      ld_R = 0;
+      if (++ld_ci == m) ld_ci = 0;
+      ld_c = c0 + ld_ci;
+    }
+    if (ld_q == 2) {  // the first real item starts at row 0 of the first cloth
+      ld_R = 0;
+      ld_ci = 0;
+      ld_c = c0;
+    }
+  };
+
+  uint64_t ph = 0;  // parity bits of this warp's waits (full[] for warp 0, lev[warp-1][] else)
+  if (warp == 0) {
+    for (int d = 0; d < kWavePrefetch; ++d) issue_next();
+    // positions 0 and 1 (the zero rows read as rows -2, -1 of the first cloth)
+    bar_wait(full_s, 0);
+    bar_wait(full_s + 8, 0);
+    ph = 3;
+  }
+
+  const uint32_t mL = 0xffffffffu;  // the lane's left edge leaves the grid only in lane 0
+  const int ix0 = FW * lane;
+  const uint32_t mLl = ix0 >= 1 ? mL : 0u;
+  const uint32_t mRt = ix0 + 4 < nx ? 0xffffffffu : 0u;
+  const bool lane_live = ix0 < nx;
+  const int64_t S = a.plane_stride;
+  // this warp's level barriers: it waits on lev[warp-1][], arrives on lev[warp][]
+  const uint32_t lev_wait = lev_s + 8u * static_cast<uint32_t>((warp > 0 ? warp - 1 : 0) * slots);
+  const uint32_t lev_mine = lev_s + 8u * static_cast<uint32_t>(warp * slots);
+
+  int q = 2;
+  int sl = 2 % slots, s1 = 1, s2 = 0;  // slots of positions q, q-1, q-2
+#pragma unroll 1
+  for (int p = 0; p < passes; ++p) {
+    const int nlev = min(W, steps - p * W);
+    if (warp >= nlev) break;  // the remaining passes are shorter still
+    const bool last = warp == nlev - 1;
+    const int k = a.k + p * W + warp;  // this warp's step index in this pass
+#pragma unroll 1
+    for (int ci = 0; ci < m; ++ci) {
+      const int b = c0 + ci;
+      const ClothConst<float> cc = a.cloths[b];
+      const bool simple = cc.n_spheres == 0 && cc.n_planes == 0;
+      const float t_next = __fmul_rn(float(k + 1), cc.dt);
+      float* const out_b = a.out + static_cast<int64_t>(b) * 6 * S;
+      float2 P0[4], P1[4], P2[4];
+      float2 Z0[2], Z1[2], Z2[2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) P0[j] = P1[j] = P2[j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) Z0[j] = Z1[j] = Z2[j] = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int R = 0; R < L; ++R) {
+        if (warp == 0) {
+          issue_next();  // position q + kWavePrefetch
+          bar_wait(full_s + 8u * static_cast<uint32_t>(sl), static_cast<uint32_t>((ph >> sl) & 1u));
+          ph ^= 1ull << sl;
+        } else if (R < ny) {
+          bar_wait(lev_wait + 8u * static_cast<uint32_t>(sl), static_cast<uint32_t>((ph >> sl) & 1u));
+          ph ^= 1ull << sl;
+        }
+        float* rowR = ring + static_cast<size_t>(sl) * ROWF;
+        float* row1 = ring + static_cast<size_t>(s1) * ROWF;
+        float* row2 = ring + static_cast<size_t>(s2) * ROWF;
+        if (R >= 2 && R < ny) {
+          row_pass<ALPHA1, false, 0, ZS>(f, rowR, row1, row2, lane, mLl, mRt, 1.f, 1.f, P0, P1,
+                                         P2, Z0, Z1, Z2);
+        } else if (R < 2) {
+          row_pass<ALPHA1, true, 0, ZS>(f, rowR, row1, row2, lane, mLl, mRt, R >= 1 ? 1.f : 0.f,
+                                        0.f, P0, P1, P2, Z0, Z1, Z2);
+        }
+        const int Rf = R - 2;
+        if (Rf >= 0) {
+          if (lane_live) {
+            float2 xs[4], vs[4];
+            float xz[4], vz[4];
+            finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
+            // in place (box column of node ix0 is ix0 + 4) or, at the last level, to HBM; the two
+            // destinations in separate branches so each store stays in its own address space
+            float* gxy = out_b + 2 * (static_cast<int64_t>(Rf) * a.pitch + ix0);
+            float* gz = out_b + 4 * S + static_cast<int64_t>(Rf) * a.pitch + ix0;
+            if (!GEN || simple) {
+              float xo[3][4], vo[3][4];
+              finish_simple(a, cc, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo);
+              if (a.health) health_simple(a.health, b, k, Rf, nx, ix0, P0, Z0, xo, vo);
+              if (last)
+                store_simple<ZS>(gxy, gxy + 2 * S, gz, gz + S, ix0, xo, vo);
+              else
+                store_simple<ZS>(row2 + XY_X + 2 * (ix0 + 4), row2 + XY_V + 2 * (ix0 + 4),
+                                 row2 + Z_X + ix0 + 4, row2 + Z_V + ix0 + 4, ix0, xo, vo);
+            } else {
+              float vo[4][3], xo[4][3];
+              uint8_t mk[4];
+              finish_general(a, cc, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
+              if (last)
+                store_general<ZS>(gxy, gxy + 2 * S, gz, gz + S, ix0, xo, vo);
+              else
+                store_general<ZS>(row2 + XY_X + 2 * (ix0 + 4), row2 + XY_V + 2 * (ix0 + 4),
+                                  row2 + Z_X + ix0 + 4, row2 + Z_V + ix0 + 4, ix0, xo, vo);
+            }
+          }
+          if (!last) bar_arrive(lev_mine + 8u * static_cast<uint32_t>(s2));  // row Rf at level warp+1
+        }
+        if (last) {
+          // the slot of position q-2 (row Rf, or a tail row of the previous cloth) is done
+          if (Rf >= 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+          bar_arrive(free_s + 8u * static_cast<uint32_t>(s2));
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          Z0[j] = Z1[j];
+          Z1[j] = Z2[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          P0[j] = P1[j];
+          P1[j] = P2[j];
+        }
+        s2 = s1;
+        s1 = sl;
+        sl = sl + 1 == slots ? 0 : sl + 1;
+        ++q;
+      }
+    }
+  }
+  // warp 0 drains nothing: every issued load was consumed (the loader stops at Q)
+}
+
+template <bool ALPHA1, int W, bool GEN, bool ZS>
+void* wave_ptr() {
+  return reinterpret_cast<void*>(wave_kernel<ALPHA1, W, GEN, ZS>);
+}
+
+template <int W>
+void* pick_wave_w(bool alpha1, bool gen, bool zs) {
+  if (gen)
+    return zs ? (alpha1 ? wave_ptr<true, W, true, true>() : wave_ptr<false, W, true, true>())
+              : (alpha1 ? wave_ptr<true, W, true, false>() : wave_ptr<false, W, true, false>());
+  return zs ? (alpha1 ? wave_ptr<true, W, false, true>() : wave_ptr<false, W, false, true>())
+            : (alpha1 ? wave_ptr<true, W, false, false>() : wave_ptr<false, W, false, false>());
+}
+
+void* pick_wave(int levels, bool alpha1, bool gen, bool zs) {
+  switch (levels) {
+    case 8: return pick_wave_w<8>(alpha1, gen, zs);
+    case 12: return pick_wave_w<12>(alpha1, gen, zs);
+    default: return pick_wave_w<16>(alpha1, gen, zs);
+  }
+}
+
+}  // namespace
+
+size_t wave_smem_bytes(int levels, int slots) {
+  return sizeof(float) * static_cast<size_t>(slots) * ROWF +
+         sizeof(uint64_t) * static_cast<size_t>(slots) * (2 + (levels - 1));
+}
+
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general) {
+  WavePlan p{};
+  p.ok = false;
+  if (nx > STRIP || ny < 2 || batch < 1) return p;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  // W = 12 levels (384 threads, 160 registers: the row pass fits without spilling; 16 levels
+  // spill at 128 registers); 8 when a cloth-pass is too short for 12 sweeps three rows apart
+  int want = 12;
+  if (const char* env = std::getenv("SC_WAVE_LEVELS")) want = std::atoi(env);
+  p.ctas = std::min(batch, sms);
+  const int m_min = batch / p.ctas;  // cloths of the least-loaded CTA
+  int slots = 0;
+  for (int levels : {16, 12, 8}) {
+    if (levels > want) continue;
+    // ring: as many slots as fit (<= 64: the per-slot parity bits live in one 64-bit word), no
+    // more than one cloth-pass of positions per CTA (a cloth's next pass must never load a row
+    // before this pass stored it), and enough for W sweeps three rows apart plus prefetch
+    int sl = 64;
+    while (sl > 0 && wave_smem_bytes(levels, sl) > static_cast<size_t>(smem_optin)) --sl;
+    sl = static_cast<int>(std::min<int64_t>(sl, static_cast<int64_t>(m_min) * (ny + 2)));
+    if (sl >= 3 * levels + kWavePrefetch + 4) {
+      p.levels = levels;
+      slots = sl;
+      break;
+    }
+  }
+  if (slots == 0) return p;
+  p.slots = slots;
+  p.smem = wave_smem_bytes(p.levels, slots);
+  p.general = general;
+  for (bool a1 : {true, false})
+    for (bool zs : {true, false})
+      cudaFuncSetAttribute(pick_wave(p.levels, a1, general, zs),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
+  p.ok = true;
+  return p;
+}
+
+cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
+                        const WavePlan& p, int steps, cudaStream_t stream) {
+  if (steps <= 0 || a.batch <= 0) return cudaSuccess;
+  void* fn = pick_wave(p.levels, f.alpha1 != 0, p.general, a.zs != 0);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.ctas));
+  cfg.blockDim = dim3(static_cast<unsigned>(32 * p.levels));
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = stream;
+  cfg.numAttrs = 0;
+  const int slots = p.slots;
+  void* args[] = {const_cast<CUtensorMap*>(&tmap[0]), const_cast<CUtensorMap*>(&tmap[1]),
+                  const_cast<StepArgs<float>*>(&a), const_cast<FastNet*>(&f),
+                  const_cast<int*>(&steps), const_cast<int*>(&slots)};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+}  // namespace scb
