@@ -65,6 +65,8 @@ struct WavePlan {
   int ctas;       // persistent CTAs (one per SM, at most one per cloth)
   size_t smem;
   bool general;   // some cloth takes the collider finish
+  int rev;        // level order reversed across warp slots (issue priority to deep levels)
+  uint32_t hint_ns;  // mbarrier try_wait suspend-time hint (0: the hardware default)
 };
 WavePlan plan_wave(int nx, int ny, int batch, int device, bool general);
 size_t wave_smem_bytes(int levels, int slots);

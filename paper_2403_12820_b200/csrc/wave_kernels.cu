@@ -46,16 +46,35 @@ constexpr int kWavePrefetch = 4;  // row positions the loader runs ahead of warp
 __device__ __forceinline__ void bar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity), "n"(1000000)
-      : "memory");
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+  if (hint_ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+  }
+}
+// an opaque copy: the compiler keeps the value in a register instead of re-deriving it (the
+// shared-window base needs an S2R of the CTA id, which it would otherwise repeat per row)
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
 }
 
 // W warps, one CTA per SM. Dynamic smem: [slots][ROWF] ring, then the barriers
@@ -64,7 +83,8 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
 template <bool ALPHA1, int W, bool GEN, bool ZS>
 __global__ void __launch_bounds__(32 * W, 1)
     wave_kernel(const __grid_constant__ CUtensorMap tmap_xy, const __grid_constant__ CUtensorMap tmap_z,
-                const StepArgs<float> a, const FastNet f, const int steps, const int slots) {
+                const StepArgs<float> a, const FastNet f, const int steps, const int slots,
+                const int rev, const uint32_t hint) {
   extern __shared__ __align__(128) float ring[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(slots) * ROWF);
   uint64_t* freeb = full + slots;
@@ -96,15 +116,16 @@ __global__ void __launch_bounds__(32 * W, 1)
   // ---- loader state (warp 0): its own cursor over (item, row) ----
   int ld_q = 0, ld_R = ny, ld_c = c0, ld_ci = 0;  // positions 0, 1: rows ny, ny+1 (OOB: zeros)
   int ld_s = 0;
-  uint64_t ph_free = 0;  // parity bits of freeb[] waits, per slot
-  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full), free_s = smem_u32(freeb);
-  const uint32_t lev_s = smem_u32(lev);
+  uint32_t ld_cyc = 0;  // ring cycle of position ld_q (its slot's barrier phases are ld_cyc & 1)
+  const uint32_t ring_s = opaque(smem_u32(ring)), full_s = opaque(smem_u32(full));
+  const uint32_t free_s = opaque(smem_u32(freeb)), lev_s = opaque(smem_u32(lev));
+  // level of this warp: warp w runs timestep w of every pass (rev: timestep W-1-w, so the
+  // hardware's issue priority of low warp slots goes to the deep levels)
+  const int lvl = rev ? W - 1 - warp : warp;
   auto issue_next = [&]() {
     if (ld_q >= Q) return;
-    if (ld_q >= slots) {  // the slot's previous row must be released by its last level
-      bar_wait(free_s + 8u * static_cast<uint32_t>(ld_s), static_cast<uint32_t>((ph_free >> ld_s) & 1u));
-      ph_free ^= 1ull << ld_s;
-    }
+    if (ld_q >= slots)  // the slot's previous position (cycle ld_cyc - 1) must be released
+      bar_wait(free_s + 8u * static_cast<uint32_t>(ld_s), (ld_cyc - 1u) & 1u, hint);
     const uint32_t dst = ring_s + static_cast<uint32_t>(ld_s) * (ROWF * 4);
     const uint32_t bar = full_s + static_cast<uint32_t>(ld_s) * 8;
     const int crow = ld_R, cb = ld_c;
@@ -129,7 +150,10 @@ __global__ void __launch_bounds__(32 * W, 1)
     }
     // advance the cursor
     ++ld_q;
-    ld_s = ld_s + 1 == slots ? 0 : ld_s + 1;
+    if (++ld_s == slots) {
+      ld_s = 0;
+      ++ld_cyc;
+    }
     if (++ld_R == L) {
       ld_R = 0;
       if (++ld_ci == m) ld_ci = 0;
@@ -142,13 +166,16 @@ __global__ void __launch_bounds__(32 * W, 1)
     }
   };
 
-  uint64_t ph = 0;  // parity bits of this warp's waits (full[] for warp 0, lev[warp-1][] else)
-  if (warp == 0) {
+  // Every barrier completes exactly once per ring cycle of its slot: the loader fills every
+  // position, each level arrives for every position q-2 at position q (finished row or zero
+  // tail row), the last level frees every position. So the phase a wait needs is the parity of
+  // the position's ring cycle (a waiter never runs a whole cycle ahead of its producer: the ring
+  // bounds the distance between levels).
+  if (lvl == 0) {
     for (int d = 0; d < kWavePrefetch; ++d) issue_next();
     // positions 0 and 1 (the zero rows read as rows -2, -1 of the first cloth)
-    bar_wait(full_s, 0);
-    bar_wait(full_s + 8, 0);
-    ph = 3;
+    bar_wait(full_s, 0, hint);
+    bar_wait(full_s + 8, 0, hint);
   }
 
   const uint32_t mL = 0xffffffffu;  // the lane's left edge leaves the grid only in lane 0
@@ -158,17 +185,18 @@ __global__ void __launch_bounds__(32 * W, 1)
   const bool lane_live = ix0 < nx;
   const int64_t S = a.plane_stride;
   // this warp's level barriers: it waits on lev[warp-1][], arrives on lev[warp][]
-  const uint32_t lev_wait = lev_s + 8u * static_cast<uint32_t>((warp > 0 ? warp - 1 : 0) * slots);
-  const uint32_t lev_mine = lev_s + 8u * static_cast<uint32_t>(warp * slots);
+  const uint32_t lev_wait = lev_s + 8u * static_cast<uint32_t>((lvl > 0 ? lvl - 1 : 0) * slots);
+  const uint32_t lev_mine = lev_s + 8u * static_cast<uint32_t>(lvl * slots);
 
   int q = 2;
   int sl = 2 % slots, s1 = 1, s2 = 0;  // slots of positions q, q-1, q-2
+  uint32_t cyc = 0;                     // ring cycle of position q
 #pragma unroll 1
   for (int p = 0; p < passes; ++p) {
     const int nlev = min(W, steps - p * W);
-    if (warp >= nlev) break;  // the remaining passes are shorter still
-    const bool last = warp == nlev - 1;
-    const int k = a.k + p * W + warp;  // this warp's step index in this pass
+    if (lvl >= nlev) break;  // the remaining passes are shorter still
+    const bool last = lvl == nlev - 1;
+    const int k = a.k + p * W + lvl;  // this warp's step index in this pass
 #pragma unroll 1
     for (int ci = 0; ci < m; ++ci) {
       const int b = c0 + ci;
@@ -184,13 +212,13 @@ __global__ void __launch_bounds__(32 * W, 1)
       for (int j = 0; j < 2; ++j) Z0[j] = Z1[j] = Z2[j] = make_float2(0.f, 0.f);
 #pragma unroll 1
       for (int R = 0; R < L; ++R) {
-        if (warp == 0) {
+        if (lvl == 0) {
           issue_next();  // position q + kWavePrefetch
-          bar_wait(full_s + 8u * static_cast<uint32_t>(sl), static_cast<uint32_t>((ph >> sl) & 1u));
-          ph ^= 1ull << sl;
+          bar_wait(full_s + 8u * static_cast<uint32_t>(sl), cyc & 1u, hint);
         } else if (R < ny) {
-          bar_wait(lev_wait + 8u * static_cast<uint32_t>(sl), static_cast<uint32_t>((ph >> sl) & 1u));
-          ph ^= 1ull << sl;
+          // tail rows are zeros the loader wrote (seen through level 0's wait chain); their
+          // barrier phases still complete (arrivals below), keeping the cycle parity
+          bar_wait(lev_wait + 8u * static_cast<uint32_t>(sl), cyc & 1u, hint);
         }
         float* rowR = ring + static_cast<size_t>(sl) * ROWF;
         float* row1 = ring + static_cast<size_t>(s1) * ROWF;
@@ -210,30 +238,34 @@ __global__ void __launch_bounds__(32 * W, 1)
             finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
             // in place (box column of node ix0 is ix0 + 4) or, at the last level, to HBM; the two
             // destinations in separate branches so each store stays in its own address space
-            float* gxy = out_b + 2 * (static_cast<int64_t>(Rf) * a.pitch + ix0);
-            float* gz = out_b + 4 * S + static_cast<int64_t>(Rf) * a.pitch + ix0;
             if (!GEN || simple) {
               float xo[3][4], vo[3][4];
               finish_simple(a, cc, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo);
               if (a.health) health_simple(a.health, b, k, Rf, nx, ix0, P0, Z0, xo, vo);
-              if (last)
+              if (last) {
+                float* gxy = out_b + 2 * (static_cast<int64_t>(Rf) * a.pitch + ix0);
+                float* gz = out_b + 4 * S + static_cast<int64_t>(Rf) * a.pitch + ix0;
                 store_simple<ZS>(gxy, gxy + 2 * S, gz, gz + S, ix0, xo, vo);
-              else
+              } else
                 store_simple<ZS>(row2 + XY_X + 2 * (ix0 + 4), row2 + XY_V + 2 * (ix0 + 4),
                                  row2 + Z_X + ix0 + 4, row2 + Z_V + ix0 + 4, ix0, xo, vo);
             } else {
               float vo[4][3], xo[4][3];
               uint8_t mk[4];
               finish_general(a, cc, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
-              if (last)
+              if (last) {
+                float* gxy = out_b + 2 * (static_cast<int64_t>(Rf) * a.pitch + ix0);
+                float* gz = out_b + 4 * S + static_cast<int64_t>(Rf) * a.pitch + ix0;
                 store_general<ZS>(gxy, gxy + 2 * S, gz, gz + S, ix0, xo, vo);
-              else
+              } else
                 store_general<ZS>(row2 + XY_X + 2 * (ix0 + 4), row2 + XY_V + 2 * (ix0 + 4),
                                   row2 + Z_X + ix0 + 4, row2 + Z_V + ix0 + 4, ix0, xo, vo);
             }
           }
-          if (!last) bar_arrive(lev_mine + 8u * static_cast<uint32_t>(s2));  // row Rf at level warp+1
         }
+        // position q-2 (row Rf in place, or a zero tail row) is ready for the next level; in the
+        // last pass the next level may be idle (its barrier then simply keeps completing)
+        if (lvl + 1 < W) bar_arrive(lev_mine + 8u * static_cast<uint32_t>(s2));
         if (last) {
           // the slot of position q-2 (row Rf, or a tail row of the previous cloth) is done
           if (Rf >= 0) asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -251,7 +283,10 @@ __global__ void __launch_bounds__(32 * W, 1)
         }
         s2 = s1;
         s1 = sl;
-        sl = sl + 1 == slots ? 0 : sl + 1;
+        if (++sl == slots) {
+          sl = 0;
+          ++cyc;
+        }
         ++q;
       }
     }
@@ -319,6 +354,10 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general) {
   }
   if (slots == 0) return p;
   p.slots = slots;
+  p.rev = 0;
+  p.hint_ns = 0;
+  if (const char* env = std::getenv("SC_WAVE_REV")) p.rev = std::atoi(env);
+  if (const char* env = std::getenv("SC_WAVE_HINT")) p.hint_ns = static_cast<uint32_t>(std::atoi(env));
   p.smem = wave_smem_bytes(p.levels, slots);
   p.general = general;
   for (bool a1 : {true, false})
@@ -340,9 +379,11 @@ cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtens
   cfg.stream = stream;
   cfg.numAttrs = 0;
   const int slots = p.slots;
+  int rev = p.rev;
+  uint32_t hint = p.hint_ns;
   void* args[] = {const_cast<CUtensorMap*>(&tmap[0]), const_cast<CUtensorMap*>(&tmap[1]),
                   const_cast<StepArgs<float>*>(&a), const_cast<FastNet*>(&f),
-                  const_cast<int*>(&steps), const_cast<int*>(&slots)};
+                  const_cast<int*>(&steps), const_cast<int*>(&slots), &rev, &hint};
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
