@@ -5,23 +5,33 @@ Metric (BASELINE.json): cloth node-updates/s (nodes x timesteps / s), whole job 
 and the fraction of the HBM roofline (48 algorithmic bytes per node-update: fp32 x and v read
 once and written once per timestep).
 
-Workload (N=1 and per rank under torchrun): BASELINE config 2 — 64 independent 256x256 cloths,
-top row pinned, gravity + per-cloth wind, dt = 1/240, the reference's 12-channel cell with
-N(0, 0.05) weights (SURVEY.md §8(d) mapping). One bench "step" = one timestep of the whole
-batch (one fused-kernel launch). Multi-GPU: every rank owns its own 64 cloths (cloth ids
-64*rank .. 64*rank+63 of the same seeded stream), no data-path collective -> weak scaling.
+Workload: BASELINE config 5 by default — 4096 independent 128x128 cloths, mixed boundary
+conditions (top row pinned / two top corners / free onto the plane z = -0.5), gravity + per-cloth
+wind, dt = 1/240, 300 timesteps, the reference's 12-channel cell with N(0, 0.05) weights
+(SURVEY.md §8(d) mapping); it is the largest single-GPU config and the one BASELINE quotes its
+1/2/4/8-GPU sweep on. `--config 2|3|4|1` runs the others. One bench "step" = one timestep of
+the whole batch; the K timed steps run device-resident (config 5: one wavefront launch that
+advances all K timesteps, csrc/wave_kernels.cu).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (one process per GPU): configs 2 and 5 shard the fixed batch B/G per rank (strong
+scaling, no data-path collective; `--scaling weak` gives every rank the whole batch instead),
+config 4 splits its 8192^2 cloth into row strips with a 2-row halo exchange per step over NCCL;
+configs 1 and 3 are replicas only. `--gpus N` without an outer torchrun spawns the N ranks
+itself and fails when fewer GPUs are visible.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref: the unmodified
-reference sources, benchmark_net's own timer) cloth-parallel on all host cores, on bounded
-samples of the same workload; under torchrun only rank 0 runs it.
+reference sources, benchmark_net's own timer) on all host cores, on bounded samples of the same
+config, with inputs built on the checker side (oracle/workloads.py: the product library is never
+loaded); under torchrun only rank 0 runs it.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,7 +42,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_NODE_UPDATE = 48  # fp32 x, v: 24 B read + 24 B written per node per timestep
-CONFIG_ID = 2  # default workload; --config 4 (row strips) / 5 (4096 cloths) also run
+DEFAULT_CONFIG = 5
+WORKLOAD_KEY = {1: "cfg1_32x32", 2: "cfg2_64x256x256", 3: "cfg3_1024x1024", 4: "cfg4_8192x8192",
+                5: "cfg5_4096x128x128"}
 
 
 def _peaks():
@@ -45,8 +57,9 @@ def _peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled every 10 ms (NVML, in-process) during the timed
-    region; falls back to nvidia-smi polling when NVML is unavailable."""
+    """SM clocks + throttle reasons during the timed region: one NVML sample when the region
+    opens, one every 10 ms from a thread while it runs, one when it closes (so even a region
+    shorter than the sampling period is covered); nvidia-smi polling when NVML is unavailable."""
 
     REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -59,49 +72,57 @@ class ClockSampler:
         self.samples = []  # (sm_mhz, max_mhz, set(reasons))
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
+        self._nv = None
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                active = {name for name, const in self.REASONS if r & getattr(nv, const)}
-                self.samples.append((float(sm), float(mx), active))
-                self._stop.wait(0.01)
-            nv.nvmlShutdown()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._max = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
         except Exception:
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(
-                        ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
-                         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                    v = [x.strip() for x in out.stdout.strip().split(",")]
-                    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                             "sw_power_cap"]
-                    self.samples.append((float(v[0]), float(v[1]),
-                                         {names[i] for i in range(4) if v[2 + i].lower() == "active"}))
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
+            self._nv = None
+
+    def sample(self):
+        if self._nv is not None:
+            nv = self._nv
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                active = {name for name, const in self.REASONS if r & getattr(nv, const)}
+                self.samples.append((float(sm), self._max, active))
+                return
+            except Exception:
+                pass
+        try:
+            out = subprocess.run(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            v = [x.strip() for x in out.stdout.strip().split(",")]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            self.samples.append((float(v[0]), float(v[1]),
+                                 {names[i] for i in range(4) if v[2 + i].lower() == "active"}))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.wait(0.01 if self._nv is not None else 0.2):
+            self.sample()
 
     def __enter__(self):
+        self.sample()
         self._t.start()
-        time.sleep(0.02)
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        self.sample()
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_min_mhz": min(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
@@ -110,23 +131,50 @@ class ClockSampler:
 
 
 def _dist():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", "0"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
-def _traffic(kernel: str, workload: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(args) -> int:
+    """--gpus N without an outer torchrun: launch the N ranks ourselves (same arguments)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": "bench.py --gpus %d: only %d GPU(s) visible; refusing to "
+                          "measure fewer ranks than asked" % (args.gpus, have)}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+           "--master-port=%d" % _free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _traffic(kernel: str, workload: str, steps: int):
+    """DRAM bytes per node-update of the dominant kernel from the committed ncu capture
+    (profiles/traffic.json: the bench's own launch). For the wavefront kernel the state crosses
+    HBM once per pass of W timesteps, so the capture's bytes per (node x pass) are rescaled to
+    this launch's ceil(K / W) passes."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(workload) if kernel == "fast_step_kernel" else t.get(kernel + ":" + workload)
-        if e and e.get("workload") == workload:
-            return e.get("dram_bytes_per_launch")
+        e = t.get("%s:%s" % (kernel, workload))
+        if not e:
+            return None, None
+        if kernel == "wave_kernel":
+            W = e["levels"]
+            per_node_pass = e["dram_bytes"] / (e["nodes"] * -(-e["steps"] // W))
+            return per_node_pass * -(-steps // W) / steps, e.get("source")
+        return e["dram_bytes"] / e["node_updates"], e.get("source")
     except Exception:
-        pass
-    return None
+        return None, None
 
 
 def _cpu_cores() -> int:
@@ -136,62 +184,74 @@ def _cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+# ------------------------------------------------------------------ reference CPU path ------
 _REF_INPUTS = {}
 
 
-def reference_sample(ref, cores: int, steps: int, warmup: int = 1, cloth0: int = 0):
-    """benchmark_net (eval.cpp:155-158) on `cores` config-2 cloths, one thread each (the
-    cloth-parallel variant: reference code unchanged, global thread count 1). Inputs are
-    generated once per (cores, cloth0) and reused across samples."""
-    from paper_2403_12820_b200 import configs
+def reference_sample(ref, cid: int, cores: int, steps: int, warmup: int = 1):
+    """benchmark_net (eval.cpp:155-158) on a bounded sample of config `cid`, inputs from the
+    checker-side generator (oracle/workloads.py). Batched configs: `cores` cloths, one
+    std::thread each (the cloth-parallel variant: reference code unchanged, global thread count
+    1). Single-cloth configs: the one cloth, node-parallel on `cores` threads (the reference's
+    own parallel_for). Returns (node-updates, seconds, description)."""
+    from oracle import workloads as W
     import numpy as np
 
-    key = (cores, cloth0)
-    if key not in _REF_INPUTS:
-        cfg, scenes, p, x, v = configs.build(CONFIG_ID, batch=cores, cloth0=cloth0)
-        keep: list = []
-        cds = [s.cloth_desc(keep) for s in scenes]
-        _REF_INPUTS[key] = (cfg, cds, keep, p.to_c(), np.ascontiguousarray(x, np.float64),
+    w = W.WORKLOADS[cid]
+    if cid not in _REF_INPUTS:
+        nb = cores if w.batch > 1 else 1
+        # no plane collider in the reference (io.cpp:321-322): config 5's free cloths fall freely
+        _, cds, keep, pc, x, v = W.build(cid, batch=nb, plane=False)
+        _REF_INPUTS[cid] = (cds, keep, pc, np.ascontiguousarray(x, np.float64),
                             np.ascontiguousarray(v, np.float64))
-    cfg, cds, _, pc, x64, v64 = _REF_INPUTS[key]
-    mx, wall = ref.benchmark_net_cloth_parallel(cfg.n, cfg.n, cds, pc, x64, v64, steps, warmup)
-    nodes = cores * cfg.n * cfg.n * steps
-    return nodes, mx, wall
+    cds, _, pc, x64, v64 = _REF_INPUTS[cid]
+    n = w.n
+    if w.batch > 1:
+        mx, _ = ref.benchmark_net_cloth_parallel(n, n, cds, pc, x64, v64, steps, warmup)
+        return len(cds) * n * n * steps, mx, "%d cloths x %d timesteps, cloth-parallel" % (
+            len(cds), steps)
+    sec = ref.benchmark_net(n, n, cds[0], pc, x64[0], v64[0], steps, warmup, threads=cores)
+    return n * n * steps, sec, "1 cloth x %d timesteps, node-parallel on %d threads" % (steps, cores)
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    from oracle.pyoracle import Reference
-    from paper_2403_12820_b200 import configs
+    from oracle.pyoracle import REF_SO, Reference
+    from oracle import workloads as W
 
-    cfg = configs.CONFIGS[CONFIG_ID]
+    cid = args.config
+    w = W.WORKLOADS[cid]
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return 0
     ref = Reference()
     cores = _cpu_cores()
-    # size every step's sample so the whole --steps K --warmup W run takes ~args.ref_budget
-    # seconds of CPU time (each step: `cores` cloths x ts timesteps, ts >= 1)
-    n0, s0, _ = reference_sample(ref, cores, 2, 1)
-    per_ts = s0 / 2
+    n0, s0, _ = reference_sample(ref, cid, cores, 1, 0)
+    per_ts = s0
     per_step = args.ref_budget / max(1, args.steps + args.warmup)
-    ts = max(1, min(200, int(per_step / max(per_ts, 1e-6))))
+    ts = max(1, min(w.steps, int(per_step / max(per_ts, 1e-6))))
     for _ in range(args.warmup):
-        reference_sample(ref, cores, ts, 0)
-    total_nodes, total_sec, times = 0, 0.0, []
+        reference_sample(ref, cid, cores, ts, 0)
+    total_nodes, total_sec = 0, 0.0
+    desc = ""
     for _ in range(args.steps):
-        n, sec, _ = reference_sample(ref, cores, ts, 0)
+        n, sec, desc = reference_sample(ref, cid, cores, ts, 0)
         total_nodes += n
         total_sec += sec
-        times.append(sec)
     value = total_nodes / total_sec
-    sample = ("%d cloths x %d timesteps of config 2 (256x256) per step, one std::thread per "
-              "cloth, reference benchmark_net timer" % (cores, ts))
+    sample = ("each step: %s of config %d (%dx%d), reference benchmark_net timer%s"
+              % (desc, cid, w.n, w.n, "; free cloths without the plane collider (the reference "
+                 "has none)" if cid == 5 else ""))
     line = {
         "impl": "reference", "metric": "cloth node-updates/s", "value": value,
-        "unit": "node-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_sec / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.description, "grid": "256x256", "cloths_sampled": cores,
-                   "timesteps_per_sample": ts, "parallelism": "cpu cloth-parallel"},
+        "unit": "node-updates/s", "n_gpus": max(world, args.gpus), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_sec / args.steps,
+        "higher_is_better": True, "scaling": "strong" if cid in (2, 4, 5) else "replicas",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "grid": "%dx%d" % (w.n, w.n),
+                   "sampled": desc, "same_config": False,
+                   "parallelism": "cpu, %d host threads" % cores},
         "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": cores,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0,
@@ -201,7 +261,26 @@ def run_reference(args, world, rank):
     return 0
 
 
-def _e2e_batch(cb, x, v, steps, mode, world, max_over_ranks, barrier, calls):
+def cpu_baseline(cid: int, seconds: float):
+    """The reference CPU path timed on this host (rank 0, N = 1), a ~`seconds` sample."""
+    try:
+        from oracle.pyoracle import Reference
+        ref = Reference()
+        cores = _cpu_cores()
+        _, s0, _ = reference_sample(ref, cid, cores, 1, 1)
+        ts = max(1, min(4000, int(seconds / max(s0, 1e-6))))
+        n, s, desc = reference_sample(ref, cid, cores, ts, 1)
+        return {"value": n / s, "unit": "node-updates/s", "cores": cores, "kind": "reference",
+                "sample": "%s of config %d, reference benchmark_net timer, %.1f s%s" % (
+                    desc, cid, s, "; free cloths without the plane (none in the reference)"
+                    if cid == 5 else "")}
+    except Exception as e:  # the box may lack the prebuilt reference library
+        return {"value": None, "unit": "node-updates/s", "cores": _cpu_cores(),
+                "kind": "reference", "sample": "unavailable: %s" % e}
+
+
+# ------------------------------------------------------------------ our GPU path ------------
+def _e2e_batch(cb, x, v, steps, barrier, max_over_ranks, calls):
     """The reference-facing C-ABI call with host buffers: sc_rollout of `steps` timesteps from
     pinned host x0/v0 to host x/v (H2D + steps + D2H inside the timed region)."""
     import ctypes as C
@@ -220,13 +299,13 @@ def _e2e_batch(cb, x, v, steps, mode, world, max_over_ranks, barrier, calls):
     arrs = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), shape=x.shape) for p in bufs]
     arrs[0][...] = x
     arrs[1][...] = v
-    cb.rollout(arrs[0], arrs[1], 2, 0, mode)  # warm the path
+    rc = lib.sc_rollout(cb.h, bufs[0], bufs[1], 2, 0, 1, bufs[2], bufs[3], None)  # warm
+    assert rc == 0, lib.sc_last_error()
     barrier()
     t = []
     for _ in range(calls):
         t0 = time.perf_counter()
-        rc = lib.sc_rollout(cb.h, bufs[0], bufs[1], steps, 0, 1 if mode == "fast" else 0,
-                            bufs[2], bufs[3], None)
+        rc = lib.sc_rollout(cb.h, bufs[0], bufs[1], steps, 0, 1, bufs[2], bufs[3], None)
         t.append(time.perf_counter() - t0)
         assert rc == 0, lib.sc_last_error()
     barrier()
@@ -262,14 +341,21 @@ def run_ours(args, world, rank, local):
 
     cid = args.config
     cfg = configs.CONFIGS[cid]
+    K = args.steps
     mode = args.mode
     peak, peak_src = _peaks()
-    kernel = "fast_step_kernel" if mode == "fast" else "parity_kernel"
     extra = {}
-    if cid in (2, 5):
-        # ---- batch sharding: every rank owns the config's batch (cloth ids B*rank ..) ----
-        B = cfg.batch
-        _, scenes, params, x, v = configs.build(cid, batch=B, cloth0=rank * B)
+    if cid != 4:
+        # ---- independent cloths: a B/G shard per rank (strong), the whole batch per rank (weak),
+        # or replicas of a single-cloth config ----
+        if cfg.batch > 1 and args.scaling == "strong":
+            b0, b1 = cfg.batch * rank // world, cfg.batch * (rank + 1) // world
+            scaling = "strong"
+        else:
+            b0, b1 = (cfg.batch * rank, cfg.batch * (rank + 1)) if cfg.batch > 1 else (0, 1)
+            scaling = "weak" if cfg.batch > 1 else "replicas"
+        B = b1 - b0
+        _, scenes, params, x, v = configs.build(cid, batch=B, cloth0=b0, threads=16)
         nodes_rank = B * cfg.n * cfg.n
         cb = ClothBatch(scenes, params, device=local)
         cb.set_state(x, v)
@@ -278,37 +364,41 @@ def run_ours(args, world, rank, local):
         barrier()
         launches0 = cb.launch_count()
         with ClockSampler(local) as clocks:
-            sec = cb.benchmark(args.steps, 0, mode)  # CUDA events around exactly K launches
-            cb.sync()
+            # CUDA events on the context stream around exactly the K timed timesteps
+            sec = cb.benchmark(K, 0, mode)
         launches = cb.launch_count() - launches0
         barrier()
         sec_max = max_over_ranks(sec)
-        # one timestep = the fused kernel over the whole batch, issued as `chunks` concurrent
-        # cloth-chunk launches (capi.cu chunked_fast_steps); its average duration over the timed
-        # region is region / steps (inter-launch gaps included, i.e. conservative)
-        avg_launch_s = sec / args.steps
-        extra["launches_per_step"] = launches / args.steps
+        kernel = ("wave_kernel" if launches == 1 and mode == "fast" else
+                  "fast_step_kernel" if mode == "fast" else "parity_kernel")
+        launch_s = sec / max(1, launches)
+        per_launch_nu = nodes_rank * K / max(1, launches)
         cb.set_state(x, v)
-        ps = max(5, min(args.steps, 20))
-        parity_value = world * nodes_rank * ps / cb.benchmark(ps, 2, "parity")
-        extra["parity_mode"] = {"value": parity_value, "unit": "node-updates/s",
-                                "note": "bit-exact with the reference f32 templates"}
-        e2e_steps = cfg.steps
-        e2e_sec, hb, db, finite = _e2e_batch(cb, x, v, e2e_steps, mode, world, max_over_ranks,
-                                             barrier, args.e2e_calls)
-        e2e = {"value": world * nodes_rank * e2e_steps / e2e_sec, "unit": "node-updates/s",
-               "h2d_bytes_per_step": hb / e2e_steps, "d2h_bytes_per_step": db / e2e_steps,
-               "call": "sc_rollout host->host, %d timesteps per call (pinned buffers)"
-                       % e2e_steps, "finite": finite}
+        ps = max(3, min(K, 10))
+        extra["parity_mode"] = {
+            "value": world * nodes_rank * ps / cb.benchmark(ps, 1, "parity") if scaling != "replicas"
+            else nodes_rank * ps / cb.benchmark(ps, 1, "parity"),
+            "unit": "node-updates/s", "note": "bit-exact with the reference f32 templates"}
+        e2e_sec, hb, db, finite = _e2e_batch(cb, x, v, K, barrier, max_over_ranks, args.e2e_calls)
+        total_nodes = world * nodes_rank if scaling != "replicas" else nodes_rank
+        if scaling == "strong":
+            total_nodes = cfg.batch * cfg.n * cfg.n
+        e2e = {"value": total_nodes * K / e2e_sec, "unit": "node-updates/s",
+               "h2d_bytes_per_step": hb / K, "d2h_bytes_per_step": db / K,
+               "call": "sc_rollout host->host, %d timesteps per call (pinned buffers)" % K,
+               "finite": finite}
         cb.close()
-        conf = {"workload": "cfg%d: %s" % (cid, cfg.description), "cloths_per_gpu": B,
-                "grid": "%dx%d" % (cfg.n, cfg.n), "nodes_per_gpu": nodes_rank,
+        conf = {"workload": "cfg%d: %s" % (cid, cfg.description), "cloths": cfg.batch,
+                "cloths_per_gpu": B, "grid": "%dx%d" % (cfg.n, cfg.n), "nodes_per_gpu": nodes_rank,
                 "timesteps_per_step": 1, "mode": mode,
-                "l2": "no flush: ping-pong state 2 x %.1f MB > 126 MB L2" % (24e-6 * nodes_rank),
-                "parallelism": "dp%d batch-sharded, no collective" % world}
-        scaling = "weak"
-    elif cid == 4:
+                "l2": "no flush: state %.1f MB per GPU%s" % (
+                    24e-6 * nodes_rank, " > 126 MB L2" if 24e-6 * nodes_rank > 126 else
+                    " (L2-resident: configs 1/3 are small by definition)"),
+                "parallelism": ("dp%d: %d cloths per GPU, no collective" % (world, B)
+                                if scaling != "replicas" else "replicas only (one cloth)")}
+    else:
         # ---- one 8192^2 cloth in row strips, halo rows over NCCL each step ----
+        scaling = "strong"
         row0, rows = strips.strip_bounds(cfg.n, world, rank)
         g0, g1 = strips.local_window(cfg.n, row0, rows)
         xl, _ = configs.sheet(cfg.seed, 0, cfg.n, g0, g1 - g0)
@@ -317,14 +407,16 @@ def run_ours(args, world, rank, local):
         sr = strips.StripRollout(scene, params, xl, np.zeros_like(xl), rank, world, local,
                                  mode=mode, transport=args.transport if mode == "fast" else "nccl")
         nodes_rank = rows * cfg.n
+        total_nodes = cfg.n * cfg.n
         for k in range(args.warmup):
             sr.step(k)
+        sr.stream.synchronize()
         barrier()
         l0 = sr.ctx.launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clocks:
             ev0.record(sr.stream)
-            for k in range(args.warmup, args.warmup + args.steps):
+            for k in range(args.warmup, args.warmup + K):
                 sr.step(k)
             ev1.record(sr.stream)
             ev1.synchronize()
@@ -332,17 +424,20 @@ def run_ours(args, world, rank, local):
         barrier()
         sec = ev0.elapsed_time(ev1) * 1e-3
         sec_max = max_over_ranks(sec)
-        avg_launch_s = sec / args.steps  # one interior launch dominates each step
+        kernel = "fast_step_kernel" if mode == "fast" else "parity_kernel"
+        launch_s = sec / K  # one interior launch dominates each step
+        per_launch_nu = nodes_rank
+        barrier()
         t0 = time.perf_counter()
         sr.ctx.set_state(xl, np.zeros_like(xl))
-        for k in range(args.steps):
+        for k in range(K):
             sr.step(k)
         sr.state()
         e2e_sec = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": world * nodes_rank * args.steps / e2e_sec, "unit": "node-updates/s",
-               "h2d_bytes_per_step": 2 * xl.nbytes / args.steps,
-               "d2h_bytes_per_step": 2 * xl.nbytes / args.steps,
-               "call": "set_state (host) + %d strip steps + get_state (host)" % args.steps}
+        e2e = {"value": total_nodes * K / e2e_sec, "unit": "node-updates/s",
+               "h2d_bytes_per_step": 2 * xl.nbytes / K,
+               "d2h_bytes_per_step": 2 * xl.nbytes / K,
+               "call": "set_state (host) + %d strip steps + get_state (host)" % K}
         sr.close()
         conf = {"workload": "cfg4: " + cfg.description, "grid": "8192x8192",
                 "nodes_per_gpu": nodes_rank, "timesteps_per_step": 1, "mode": mode,
@@ -350,44 +445,28 @@ def run_ours(args, world, rank, local):
                 "parallelism": "%d row strips, 2-row halo per step %s" % (
                     world, "stored into the neighbours' ghost rows over peer memory (fused)"
                     if sr.transport == "peer" else "over NCCL")}
-        scaling = "strong"
-    else:
-        raise SystemExit("--config must be 2, 4 or 5")
 
-    value = world * nodes_rank * args.steps / sec_max if cid != 4 else \
-        cfg.n * cfg.n * args.steps / sec_max
-    achieved = BYTES_PER_NODE_UPDATE * nodes_rank / avg_launch_s / 1e9
-    workload = {2: "cfg2_64x256x256", 4: "cfg4_8192x8192", 5: "cfg5_4096x128x128"}[cid]
+    value = total_nodes * K / sec_max
+    achieved = BYTES_PER_NODE_UPDATE * per_launch_nu / launch_s / 1e9
+    traffic_per_nu, traffic_src = _traffic(kernel, WORKLOAD_KEY[cid], K)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _traffic(kernel, workload),
-                "kernel": kernel, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": BYTES_PER_NODE_UPDATE * nodes_rank,
-                "avg_launch_ms": avg_launch_s * 1e3,
-                "per": "timestep of the whole batch (its cloth-chunk launches run concurrently)"}
+                "frac": achieved / peak,
+                "traffic": traffic_per_nu * per_launch_nu if traffic_per_nu else None,
+                "traffic_source": traffic_src, "kernel": kernel, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": BYTES_PER_NODE_UPDATE * per_launch_nu,
+                "avg_launch_ms": launch_s * 1e3,
+                "per": ("one launch advancing all %d timed timesteps of this GPU's cloths" % K
+                        if kernel == "wave_kernel" else "one timestep (launch) of this GPU's share")}
 
-    # ---- CPU baseline: reference CPU path on this host, bounded sample (rank 0, N=1) ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and cid == 2:
-        try:
-            from oracle.pyoracle import Reference
-            ref = Reference()
-            cores = _cpu_cores()
-            n0, s0, _ = reference_sample(ref, cores, 2, 1)
-            ts = max(1, min(4000, int(args.cpu_seconds / max(s0 / 2, 1e-6))))
-            n, s, wall = reference_sample(ref, cores, ts, 1)
-            cpu = {"value": n / s, "unit": "node-updates/s", "cores": cores, "kind": "reference",
-                   "sample": "%d config-2 cloths (256x256) x %d timesteps, cloth-parallel "
-                             "(one std::thread per cloth), reference benchmark_net timer, "
-                             "%.1f s" % (cores, ts, s)}
-        except Exception as e:  # the box may lack the prebuilt reference library
-            cpu = {"value": None, "unit": "node-updates/s", "cores": _cpu_cores(),
-                   "kind": "reference", "sample": "unavailable: %s" % e}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cid, args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": "cloth node-updates/s", "value": value, "unit": "node-updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * sec_max / args.steps, "higher_is_better": True,
+            "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec_max / K, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": conf, "roofline": roofline, "hbm_fraction": achieved / peak,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary(),
@@ -403,11 +482,13 @@ def run_ours(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=0, help="timed timesteps (0: the config's own)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
-    ap.add_argument("--config", type=int, choices=[2, 4, 5], default=CONFIG_ID)
+    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=DEFAULT_CONFIG)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="batched configs: fixed batch split over the GPUs, or a batch per GPU")
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
                     help="config 4 halo exchange: NCCL send/recv or the fused peer-store kernel")
@@ -418,9 +499,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.steps <= 0:
+        from oracle.workloads import WORKLOADS
+        args.steps = WORKLOADS[args.config].steps
     world, rank, local = _dist()
     if args.impl == "reference":
-        return run_reference(args, world, rank)
+        return run_reference(args, max(world, 1), rank)
+    if world == 0:
+        if args.gpus > 1:
+            return _spawn(args)
+        world = 1
+    elif world != args.gpus:
+        print("bench.py: WORLD_SIZE=%d overrides --gpus %d" % (world, args.gpus), file=sys.stderr)
     return run_ours(args, world, rank, local)
 
 

@@ -16,7 +16,28 @@ from typing import Optional
 
 import numpy as np
 
-from paper_2403_12820_b200 import _abi
+
+def _load_abi_types():
+    """The C-ABI struct layouts (paper_2403_12820_b200/_abi.py) loaded as a standalone module:
+    importing the package would load libstencilcloth_b200.so, and the checker side (tests'
+    oracle, bench.py's reference arm) must run without the product library."""
+    import importlib.util
+    import sys
+    # registered under its package name, so a later `import paper_2403_12820_b200` reuses this
+    # very module (one set of ctypes classes for both sides)
+    name = "paper_2403_12820_b200._abi"
+    if name in sys.modules:
+        return sys.modules[name]
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_2403_12820_b200", "_abi.py")
+    spec = importlib.util.spec_from_file_location(name, path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+_abi = _load_abi_types()
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")

@@ -130,6 +130,7 @@ struct sc_ctx {
   FastPlan plan{};       // simple finish (no colliders / pressure / mask)
   FastPlan plan_gen{};   // general finish
   WavePlan wave{};       // wavefront temporal blocking (nx <= 128 batches, no pressure plug)
+  std::map<int, WavePlan> wave_chunk;  // plans for cloth-chunk launches (pipelined rollout)
   bool wave_on = true;   // sc_ctx_set_persistent / SC_WAVE=0: the streaming kernel only
   bool wave_pinned = false;
   std::map<long long, FastPlan> plan_cache;  // row-range launches of strip contexts
@@ -186,6 +187,7 @@ void free_scene(sc_ctx* c) {
   c->has_scene = false;
   c->tmap_ok = false;
   c->plan_cache.clear();
+  c->wave_chunk.clear();
   // a rebound scene must not keep pointers into the neighbours' (old) buffers
   for (auto& q : c->peer) {
     for (void*& o : q.opened)
@@ -773,6 +775,91 @@ bool pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// Host -> host FAST rollout of a wavefront context with the transfers overlapped: the batch goes
+// in K cloth chunks; chunk i's H2D runs on a copy stream while the compute stream converts and
+// steps the chunks before it, and its D2H on a second copy stream while the chunks after it
+// step. Each chunk is one wavefront launch over all SMs (chunks of >= 4 cloths per CTA keep
+// its load balance), so the device time is the unchunked one plus one chunk's copies.
+bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int k0,
+                            void* xo, void* vo) {
+  if (const char* env = std::getenv("SC_PIPELINE"))
+    if (std::atoi(env) == 0) return false;
+  if (!wave_usable(c) || steps < 2 || !xo || !vo) return false;
+  if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
+  int K = c->batch >= 16 * c->wave.ctas ? 4 : c->batch >= 8 * c->wave.ctas ? 2 : 1;
+  if (const char* env = std::getenv("SC_WAVE_CHUNKS")) K = std::atoi(env);  // tuning / tests
+  K = std::min(std::min(K, 4), c->batch);
+  if (K < 2) return false;
+  int b0[5];
+  for (int i = 0; i <= K; ++i) b0[i] = static_cast<int>((static_cast<int64_t>(i) * c->batch) / K);
+  for (int i = 0; i < K; ++i) {
+    const int nb = b0[i + 1] - b0[i];
+    if (c->wave_chunk.find(nb) == c->wave_chunk.end())
+      c->wave_chunk[nb] = plan_wave(c->nx, c->ny, nb, c->device, c->any_general);
+    if (!c->wave_chunk[nb].ok) return false;
+  }
+  for (int i = 0; i < 2; ++i)
+    if (!c->pipe_stream[i])
+      ck(cudaStreamCreateWithFlags(&c->pipe_stream[i], cudaStreamNonBlocking), "stream");
+  for (cudaEvent_t& e : c->pipe_ev)
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  const size_t cloth_bytes = static_cast<size_t>(c->nodes_local()) * 3 * sizeof(float);
+  const size_t bytes = cloth_bytes * c->batch;
+  c->aos.ensure(2 * bytes);
+  unsigned char* dx = c->aos.p;
+  unsigned char* dv = c->aos.p + bytes;
+  const int64_t S = c->plane_stride;
+  float* st = static_cast<float*>(c->state[c->cur]);
+  cudaStream_t in = c->pipe_stream[0], out = c->pipe_stream[1];
+  cudaEvent_t* ev_in = c->pipe_ev;          // [K]
+  cudaEvent_t* ev_out = c->pipe_ev + 8;     // [K]
+  ck(cudaEventRecord(c->pipe_ev[16], c->stream), "event");  // earlier work on the ctx stream
+  ck(cudaStreamWaitEvent(in, c->pipe_ev[16], 0), "wait");
+  for (int i = 0; i < K; ++i) {
+    const size_t off = cloth_bytes * b0[i], n = cloth_bytes * (b0[i + 1] - b0[i]);
+    ck(cudaMemcpyAsync(dx + off, static_cast<const unsigned char*>(x0) + off, n,
+                       cudaMemcpyHostToDevice, in), "H2D x");
+    ck(cudaMemcpyAsync(dv + off, static_cast<const unsigned char*>(v0) + off, n,
+                       cudaMemcpyHostToDevice, in), "H2D v");
+    ck(cudaEventRecord(ev_in[i], in), "event");
+  }
+  for (int i = 0; i < K; ++i) {
+    const int nb = b0[i + 1] - b0[i];
+    const size_t off = cloth_bytes * b0[i];
+    ck(cudaStreamWaitEvent(c->stream, ev_in[i], 0), "wait");
+    ck(launch_aos_to_planar<float>(reinterpret_cast<float*>(dx + off),
+                                   reinterpret_cast<float*>(dv + off), st + b0[i] * 6 * S, nb,
+                                   c->nx, c->rows_local, S, c->pitch, c->zs, c->stream),
+       "aos_to_planar");
+    StepArgs<float> a = base_args<float>(c);
+    a.out = st;  // in place
+    a.k = k0;
+    a.b_off = b0[i];
+    a.batch = nb;
+    a.net = c->net32;
+    a.health = c->health_on ? c->health.p : nullptr;
+    ck(launch_wave(a, c->fast, c->tmap[c->cur], c->wave_chunk[nb], steps, c->stream),
+       "kernel launch");
+    ck(launch_planar_to_aos<float>(st + b0[i] * 6 * S, reinterpret_cast<float*>(dx + off),
+                                   reinterpret_cast<float*>(dv + off), nb, c->nx, c->rows_local,
+                                   S, c->pitch, c->zs, c->stream),
+       "planar_to_aos");
+    ck(cudaEventRecord(ev_out[i], c->stream), "event");
+  }
+  for (int i = 0; i < K; ++i) {
+    const size_t off = cloth_bytes * b0[i], n = cloth_bytes * (b0[i + 1] - b0[i]);
+    ck(cudaStreamWaitEvent(out, ev_out[i], 0), "wait");
+    ck(cudaMemcpyAsync(static_cast<unsigned char*>(xo) + off, dx + off, n,
+                       cudaMemcpyDeviceToHost, out), "D2H x");
+    ck(cudaMemcpyAsync(static_cast<unsigned char*>(vo) + off, dv + off, n,
+                       cudaMemcpyDeviceToHost, out), "D2H v");
+  }
+  ck(cudaEventRecord(c->pipe_ev[16], out), "event");
+  ck(cudaStreamWaitEvent(c->stream, c->pipe_ev[16], 0), "wait");
+  c->launches.fetch_add(3 * K);
+  return true;
+}
+
 bool rollout_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int k0, void* xo,
                        void* vo) {
   if (const char* env = std::getenv("SC_PIPELINE"))
@@ -1043,7 +1130,8 @@ sc_status sc_rollout(sc_ctx* c, const void* x0, const void* v0, int32_t steps, i
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     reset_health(c);
     if (!constrained && mode == SC_MODE_FAST && steps > 0 &&
-        rollout_pipelined(c, x0, v0, steps, k0, x_out, v_out)) {
+        (rollout_wave_pipelined(c, x0, v0, steps, k0, x_out, v_out) ||
+         rollout_pipelined(c, x0, v0, steps, k0, x_out, v_out))) {
       ck(cudaStreamSynchronize(c->stream), "sync");
       return;
     }

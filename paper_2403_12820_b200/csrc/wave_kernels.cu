@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(32 * W, 1)
   __syncthreads();
 
   // this CTA's cloths [c0, c0 + m)
-  const int B = a.batch;
-  const int c0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * B / gridDim.x);
-  const int m = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * B / gridDim.x) - c0;
+  const int B = a.batch;  // cloths [a.b_off, a.b_off + B) of the context
+  const int c0 = a.b_off + static_cast<int>(static_cast<int64_t>(blockIdx.x) * B / gridDim.x);
+  const int m = a.b_off + static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * B / gridDim.x) - c0;
   if (m <= 0) return;
   const int nx = a.nx, ny = a.ny;
   const int L = ny + 2;  // positions per (cloth, pass): rows 0..ny-1 and two zero tail rows

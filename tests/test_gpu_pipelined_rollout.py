@@ -19,6 +19,7 @@ def test_pipelined_rollout_bit_identical(monkeypatch, cfg_id, n, batch, steps):
     xp[...] = x
     vp[...] = v
     with ClothBatch(scenes, p) as cb:
+        cb.set_persistent(False)  # the streaming kernel's chunked pipeline (not the wavefront)
         xa, va = cb.rollout(x, v, steps, 3, "fast")  # pageable: plain path
         l0 = cb.launch_count()
         xo, vo = pinned_empty(x.shape), pinned_empty(v.shape)
@@ -42,6 +43,7 @@ def test_chunked_stepping_bit_identical_to_whole_batch(monkeypatch, cfg_id, n, b
     for k in ("0", "2", "4"):
         monkeypatch.setenv("SC_CHUNKS", k)
         with ClothBatch(scenes, p) as cb:
+            cb.set_persistent(False)  # streaming kernel: chunked launches per step
             cb.set_state(x, v)
             l0 = cb.launch_count()
             cb.advance(11, 0, "fast")
@@ -74,3 +76,28 @@ def test_chunked_stepping_vs_oracle(oracle):
     okx, ex = fast_close(xf, xo, 2e-5)
     okv, ev = fast_close(vf, vo, 2e-5)
     assert okx and okv, "rel err x %.3g v %.3g" % (ex, ev)
+
+
+@pytest.mark.parametrize("chunks,batch,steps", [("2", 300, 14), ("4", 600, 25), ("3", 151, 2)])
+def test_wave_pipelined_rollout_bit_identical(monkeypatch, chunks, batch, steps):
+    """The wavefront context's host -> host rollout in cloth chunks (capi.cu
+    rollout_wave_pipelined: H2D / step / D2H of different chunks overlapped) against the plain
+    path and the streaming kernel: bit-identical."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    from paper_2403_12820_b200.api import pinned_empty
+    cfg, scenes, p, x, v = configs.build(5, batch=batch, n=128)
+    xp, vp = pinned_empty(x.shape), pinned_empty(v.shape)
+    xp[...] = x
+    vp[...] = v
+    monkeypatch.setenv("SC_WAVE_CHUNKS", chunks)
+    with ClothBatch(scenes, p) as cb:
+        xa, va = cb.rollout(x, v, steps, 3, "fast")  # pageable: one wavefront launch
+        l0 = cb.launch_count()
+        xo, vo = pinned_empty(x.shape), pinned_empty(v.shape)
+        xb, vb = cb.rollout(xp, vp, steps, 3, "fast", out=(xo, vo))  # pinned: chunked, overlapped
+        lp = cb.launch_count() - l0
+        cb.set_persistent(False)
+        xc, vc = cb.rollout(x, v, steps, 3, "fast")
+    assert bits_equal(xb, xa) and bits_equal(vb, va)
+    assert bits_equal(xc, xa) and bits_equal(vc, va)
+    assert lp == 3 * int(chunks)  # layout in + wavefront + layout out per chunk
