@@ -28,14 +28,16 @@ def bits_equal(a, b):
         a.view(np.uint8), b.view(np.uint8))
 
 
-def fast_close(a, b, rtol=FAST_RTOL):
+def fast_close(a, b, rtol=FAST_RTOL, normwise=1e-6):
+    """Per component plane |a - b| <= rtol * max(|b|, rms(b)) and max|a - b| / max|b| <=
+    normwise (test_gpu_fullsize.py explains why the floor is the field's RMS)."""
     a = np.asarray(a, np.float64).reshape(-1, 3)
     b = np.asarray(b, np.float64).reshape(-1, 3)
     rms = np.sqrt(np.mean(b * b, axis=0))
     scale = np.maximum(np.abs(b), rms[None, :])
     err = np.abs(a - b)
-    ok = err <= rtol * scale
-    return bool(ok.all()), float((err / np.maximum(scale, 1e-300)).max())
+    ok = (err <= rtol * scale).all() and err.max() <= normwise * max(np.abs(b).max(), 1e-300)
+    return bool(ok), float((err / np.maximum(scale, 1e-300)).max())
 
 
 def golden_ctx(z, precision="f32"):
@@ -170,8 +172,9 @@ def test_fast_short_rollout_drift_bounded(oracle):
     with ClothBatch(scenes, p) as cb:
         xp, vp = cb.rollout(x, v, 10, 0, "parity")
         xf, vf = cb.rollout(x, v, 10, 0, "fast")
-    okx, ex = fast_close(xf, xp, 1e-4)
-    okv, ev = fast_close(vf, vp, 1e-4)
+    okx, ex = fast_close(xf, xp, 1e-5, normwise=1e-5)
+    okv, ev = fast_close(vf, vp, 1e-5, normwise=1e-5)
+    print("10-step FAST drift (rms-floored relative): x %.3g v %.3g" % (ex, ev))
     assert okx and okv, "10-step drift x %.3g v %.3g" % (ex, ev)
 
 

@@ -73,8 +73,8 @@ def test_chunked_stepping_vs_oracle(oracle):
         cb.advance(2, 3, "fast")
         assert cb.launch_count() - l0 >= 4  # 2 chunks x 2 steps
         xf, vf = cb.get_state()
-    okx, ex = fast_close(xf, xo, 2e-5)
-    okv, ev = fast_close(vf, vo, 2e-5)
+    okx, ex = fast_close(xf, xo, 1e-5, normwise=2e-6)
+    okv, ev = fast_close(vf, vo, 1e-5, normwise=2e-6)
     assert okx and okv, "rel err x %.3g v %.3g" % (ex, ev)
 
 
