@@ -72,7 +72,10 @@ class StripRollout:
     the cloth's global descriptor (global pins; positions not needed)."""
 
     def __init__(self, scene, params, x_local, v_local, rank: int, world: int, device: int = 0,
-                 group=None, mode: str = "fast", transport: str = "nccl"):
+                 group=None, mode: str = "fast", transport: str = "nccl", ctx=None):
+        """ctx: a strip context to drive instead of the GPU one (the CPU tests pass an
+        oracle-backed stand-in with the same strip_step / halo_pack / halo_unpack /
+        strip_commit surface; its halo buffers are then host tensors and there is no stream)."""
         import torch
 
         from .api import ClothBatch
@@ -86,14 +89,20 @@ class StripRollout:
         self.ny = scene.ny
         self.row0, self.rows = strip_bounds(scene.ny, world, rank)
         self.g0, self.g1 = local_window(scene.ny, self.row0, self.rows)
-        self.ctx = ClothBatch([scene], params, "f32", device, strip=(self.row0, self.rows))
+        if ctx is None:
+            self.ctx = ClothBatch([scene], params, "f32", device, strip=(self.row0, self.rows))
+            dev = torch.device("cuda", device)
+        else:
+            if self.transport == "peer":
+                raise ValueError("transport 'peer' needs the GPU context")
+            self.ctx = ctx
+            dev = torch.device("cpu")
         self.ctx.set_state(x_local, v_local)
         n = self.ctx.halo_elems()
-        dev = torch.device("cuda", device)
         self.send_lo, self.send_hi, self.recv_lo, self.recv_hi = (
             torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(4))
         # a real (non-legacy) stream: kernels, packs and NCCL all order on it
-        self.stream = torch.cuda.Stream(device=dev)
+        self.stream = torch.cuda.Stream(device=dev) if ctx is None else None
         if transport == "peer" and world > 1:
             import torch.distributed as dist
             exports = [None] * world
@@ -113,6 +122,9 @@ class StripRollout:
     def step(self, k: int) -> None:
         import torch
 
+        if self.stream is None:
+            self._step(k, None)
+            return
         with torch.cuda.stream(self.stream):
             self._step(k, self.stream.cuda_stream)
 
@@ -148,7 +160,8 @@ class StripRollout:
         self.ctx.strip_commit()
 
     def state(self):
-        self.stream.synchronize()
+        if self.stream is not None:
+            self.stream.synchronize()
         return self.ctx.get_state()
 
     def close(self) -> None:
