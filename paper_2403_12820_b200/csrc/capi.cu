@@ -131,6 +131,14 @@ struct sc_ctx {
   FastPlan plan_gen{};   // general finish
   WavePlan wave{};       // wavefront temporal blocking (nx <= 128 batches, no pressure plug)
   std::map<int, WavePlan> wave_chunk;  // plans for cloth-chunk launches (pipelined rollout)
+  // class groups (a batch mixing collider-free cloths with collider cloths): the collider-free
+  // ones through the wavefront kernel without the collider finish, the others through the
+  // streaming kernel (its general finish runs faster at its occupancy)
+  bool grouped = false;
+  int n_simple = 0, n_general = 0;
+  DevBuf<int32_t> ids_simple, ids_general;
+  WavePlan wave_simple{};
+  FastPlan plan_general{};
   bool wave_on = true;   // sc_ctx_set_persistent / SC_WAVE=0: the streaming kernel only
   bool wave_pinned = false;
   std::map<long long, FastPlan> plan_cache;  // row-range launches of strip contexts
@@ -188,6 +196,9 @@ void free_scene(sc_ctx* c) {
   c->tmap_ok = false;
   c->plan_cache.clear();
   c->wave_chunk.clear();
+  c->ids_simple.release();
+  c->ids_general.release();
+  c->grouped = false;
   // a rebound scene must not keep pointers into the neighbours' (old) buffers
   for (auto& q : c->peer) {
     for (void*& o : q.opened)
@@ -719,6 +730,45 @@ void chunked_fast_steps(sc_ctx* c, int K, int steps, int k0, Pre pre, Post post)
   if (steps & 1) c->cur = 1 - c->cur;
 }
 
+// n FAST timesteps of a class-grouped context's cloths simple ids [s0, s0 + ns) and general ids
+// [g0, g0 + ng), from buffer cur into buffer (cur + n) % 2: the collider-free cloths in one
+// wavefront launch (grid wplan.ctas: part of the SMs) on `main`, the collider cloths in n
+// ping-pong streaming launches on a side stream at the same time (they land on the SMs the
+// wavefront grid leaves free, and on all of them once it is done); `main` waits for both.
+void grouped_steps(sc_ctx* c, int n, int k0, int s0, int ns, int g0, int ng,
+                   const WavePlan& wplan, const FastPlan& gplan, cudaStream_t main) {
+  const int out = (c->cur + n) & 1;
+  if (!c->pipe_stream[2])
+    ck(cudaStreamCreateWithFlags(&c->pipe_stream[2], cudaStreamNonBlocking), "stream");
+  for (cudaEvent_t& e : c->pipe_ev)
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cudaStream_t side = c->pipe_stream[2];
+  ck(cudaEventRecord(c->pipe_ev[14], main), "event");
+  ck(cudaStreamWaitEvent(side, c->pipe_ev[14], 0), "wait");
+  StepArgs<float> a = base_args<float>(c);
+  a.net = c->net32;
+  a.health = c->health_on ? c->health.p : nullptr;
+  if (ns > 0) {
+    a.out = static_cast<float*>(c->state[out]);
+    a.k = k0;
+    a.ids = c->ids_simple.p + s0;
+    a.batch = ns;
+    ck(launch_wave(a, c->fast, c->tmap[c->cur], c->tmap[out], wplan, n, main), "kernel launch");
+  }
+  a.ids = c->ids_general.p + g0;
+  a.batch = ng;
+  for (int s2 = 0; ng > 0 && s2 < n; ++s2) {
+    const int in = (c->cur + s2) & 1;
+    a.in = static_cast<const float*>(c->state[in]);
+    a.out = static_cast<float*>(c->state[in ^ 1]);
+    a.k = k0 + s2;
+    ck(launch_fast(a, c->fast, c->tmap[in], gplan, side), "kernel launch");
+  }
+  ck(cudaEventRecord(c->pipe_ev[15], side), "event");
+  ck(cudaStreamWaitEvent(main, c->pipe_ev[15], 0), "wait");
+  c->launches.fetch_add((ns > 0 ? 1 : 0) + (ng > 0 ? n : 0));
+}
+
 void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_last,
                   int kind = KIND_STEP) {
   if (steps < 0) throw_config("steps: must be >= 0");
@@ -728,13 +778,21 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
   int s = 0;
   if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST && wave_usable(c)) {
     const int n = steps - (dev_mask_last ? 1 : 0);  // a mask-producing last step runs whole
-    if (n >= 2) {
+    if (n >= 2 && c->grouped) {
+      const int out = (c->cur + n) & 1;
+      grouped_steps(c, n, k0, 0, c->n_simple, 0, c->n_general, c->wave_simple, c->plan_general,
+                    c->stream);
+      c->cur = out;
+      k0 += n;
+      steps -= n;
+    } else if (n >= 2) {
       StepArgs<float> a = base_args<float>(c);
       a.out = static_cast<float*>(c->state[c->cur]);  // in place
       a.k = k0;
       a.net = c->net32;
       a.health = c->health_on ? c->health.p : nullptr;
-      ck(launch_wave(a, c->fast, c->tmap[c->cur], c->wave, n, c->stream), "kernel launch");
+      ck(launch_wave(a, c->fast, c->tmap[c->cur], c->tmap[c->cur], c->wave, n, c->stream),
+         "kernel launch");
       c->launches.fetch_add(1);
       k0 += n;  // the mask-producing last step (if any) follows below
       steps -= n;
@@ -792,12 +850,35 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
   if (K < 2) return false;
   int b0[5];
   for (int i = 0; i <= K; ++i) b0[i] = static_cast<int>((static_cast<int64_t>(i) * c->batch) / K);
+  // class-grouped contexts: each chunk's collider-free / collider cloths are contiguous slices
+  // of the two (ascending) id lists
+  std::vector<int> s_lo(K + 1, 0), g_lo(K + 1, 0);
+  if (c->grouped) {
+    std::vector<int32_t> ids(static_cast<size_t>(c->n_simple));
+    ck(cudaMemcpy(ids.data(), c->ids_simple.p, sizeof(int32_t) * ids.size(),
+                  cudaMemcpyDeviceToHost), "D2H ids");
+    for (int i = 0; i <= K; ++i) {
+      s_lo[i] = static_cast<int>(std::lower_bound(ids.begin(), ids.end(), b0[i]) - ids.begin());
+      g_lo[i] = b0[i] - s_lo[i];
+    }
+  }
   for (int i = 0; i < K; ++i) {
     const int nb = b0[i + 1] - b0[i];
+    if (c->grouped) {
+      const int ns = s_lo[i + 1] - s_lo[i], ng = g_lo[i + 1] - g_lo[i];
+      const int key = -1 - ns;  // grouped chunk plans: negative keys
+      if (c->wave_chunk.find(key) == c->wave_chunk.end())
+        c->wave_chunk[key] = plan_wave(c->nx, c->ny, ns, c->device, false, c->wave_simple.ctas);
+      if (ns > 0 && !c->wave_chunk[key].ok) return false;
+      if (c->plan_cache.find(-1 - ng) == c->plan_cache.end())
+        c->plan_cache[-1 - ng] = plan_fast(c->nx, c->u1 - c->u0, ng, c->device, false, true);
+      continue;
+    }
     if (c->wave_chunk.find(nb) == c->wave_chunk.end())
       c->wave_chunk[nb] = plan_wave(c->nx, c->ny, nb, c->device, c->any_general);
     if (!c->wave_chunk[nb].ok) return false;
   }
+  const int out_buf = c->grouped ? (c->cur + steps) & 1 : c->cur;
   for (int i = 0; i < 2; ++i)
     if (!c->pipe_stream[i])
       ck(cudaStreamCreateWithFlags(&c->pipe_stream[i], cudaStreamNonBlocking), "stream");
@@ -831,16 +912,24 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
                                    reinterpret_cast<float*>(dv + off), st + b0[i] * 6 * S, nb,
                                    c->nx, c->rows_local, S, c->pitch, c->zs, c->stream),
        "aos_to_planar");
-    StepArgs<float> a = base_args<float>(c);
-    a.out = st;  // in place
-    a.k = k0;
-    a.b_off = b0[i];
-    a.batch = nb;
-    a.net = c->net32;
-    a.health = c->health_on ? c->health.p : nullptr;
-    ck(launch_wave(a, c->fast, c->tmap[c->cur], c->wave_chunk[nb], steps, c->stream),
-       "kernel launch");
-    ck(launch_planar_to_aos<float>(st + b0[i] * 6 * S, reinterpret_cast<float*>(dx + off),
+    if (c->grouped) {
+      const int ns = s_lo[i + 1] - s_lo[i], ng = g_lo[i + 1] - g_lo[i];
+      grouped_steps(c, steps, k0, s_lo[i], ns, g_lo[i], ng, c->wave_chunk[-1 - ns],
+                    c->plan_cache[-1 - ng], c->stream);
+    } else {
+      StepArgs<float> a = base_args<float>(c);
+      a.out = st;  // in place
+      a.k = k0;
+      a.b_off = b0[i];
+      a.batch = nb;
+      a.net = c->net32;
+      a.health = c->health_on ? c->health.p : nullptr;
+      ck(launch_wave(a, c->fast, c->tmap[c->cur], c->tmap[c->cur], c->wave_chunk[nb], steps,
+                     c->stream),
+         "kernel launch");
+    }
+    float* fin = static_cast<float*>(c->state[out_buf]);
+    ck(launch_planar_to_aos<float>(fin + b0[i] * 6 * S, reinterpret_cast<float*>(dx + off),
                                    reinterpret_cast<float*>(dv + off), nb, c->nx, c->rows_local,
                                    S, c->pitch, c->zs, c->stream),
        "planar_to_aos");
@@ -856,7 +945,8 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
   }
   ck(cudaEventRecord(c->pipe_ev[16], out), "event");
   ck(cudaStreamWaitEvent(c->stream, c->pipe_ev[16], 0), "wait");
-  c->launches.fetch_add(3 * K);
+  c->launches.fetch_add(c->grouped ? 2 * K : 3 * K);
+  c->cur = out_buf;
   return true;
 }
 
@@ -1025,8 +1115,42 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
                           c->any_general);
       c->plan_gen = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure, true);
       c->wave = WavePlan{};
-      if (c->strip_row0 < 0 && !c->any_pressure)
+      c->grouped = false;
+      if (c->strip_row0 < 0 && !c->any_pressure) {
         c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general);
+        std::vector<int32_t> simple, general;
+        for (int b = 0; b < s->batch; ++b)
+          (s->cloths[b].n_spheres > 0 || s->cloths[b].n_planes > 0 ? general : simple).push_back(b);
+        bool want = !simple.empty() && !general.empty();
+        if (const char* env = std::getenv("SC_GROUP")) want = want && std::atoi(env) != 0;
+        if (want) {
+          // the two groups run concurrently: the wavefront kernel on part of the SMs, the
+          // streaming launches of the collider cloths on the rest. Split measured on config 5
+          // (tools/cfg5_class_probe.py, SC_GROUP_SMS sweep: 100-108 of 148 SMs best for 2731
+          // collider-free + 1365 plane cloths): SMs in proportion to 1.05 x collider-free
+          // cloths : 1 x collider cloths
+          int sms = 148;
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+          const double ws = 1.05 * simple.size(), wg = 1.0 * general.size();
+          int wave_sms = static_cast<int>(sms * ws / (ws + wg) + 0.5);
+          if (const char* env = std::getenv("SC_GROUP_SMS")) wave_sms = std::atoi(env);
+          wave_sms = std::max(1, std::min(sms, wave_sms));
+          c->wave_simple = plan_wave(c->nx, c->ny, static_cast<int>(simple.size()), c->device, false,
+                                     wave_sms);
+          if (c->wave_simple.ok) {
+            c->n_simple = static_cast<int>(simple.size());
+            c->n_general = static_cast<int>(general.size());
+            c->ids_simple.ensure(simple.size());
+            c->ids_general.ensure(general.size());
+            ck(cudaMemcpy(c->ids_simple.p, simple.data(), sizeof(int32_t) * simple.size(),
+                          cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
+            ck(cudaMemcpy(c->ids_general.p, general.data(), sizeof(int32_t) * general.size(),
+                          cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
+            c->plan_general = plan_fast(c->nx, c->u1 - c->u0, c->n_general, c->device, false, true);
+            c->grouped = true;
+          }
+        }
+      }
       if (!c->wave_pinned) {
         c->wave_on = true;
         if (const char* env = std::getenv("SC_WAVE")) c->wave_on = std::atoi(env) != 0;

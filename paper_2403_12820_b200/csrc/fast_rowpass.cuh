@@ -618,33 +618,35 @@ __device__ __forceinline__ void store_general(float* oxy, float* ovxy, float* oz
   *reinterpret_cast<float4*>(ovz) = zgroup<ZS>(ix0, vo[0][2], vo[1][2], vo[2][2], vo[3][2]);
 }
 
-// Colliders and/or the contact mask: the lane's 4 nodes together (collider outer, node inner:
-// each collider's constants are loaded once per row), each node through the same IEEE-exact
-// sequence as advance_with_impulse (sc_device.cuh), so contact decisions and masks match PARITY.
+// The first sphere and plane of a cloth, loaded once per cloth (unit / item) instead of once
+// per finished row; further colliders are read from the tables as they come.
+struct Colliders {
+  SphereConst<float> s0;
+  PlaneConst<float> p0;
+};
+__device__ __forceinline__ Colliders load_colliders(const StepArgs<float>& a,
+                                                    const ClothConst<float>& cc) {
+  Colliders c{};
+  if (cc.n_spheres > 0) c.s0 = a.spheres[cc.sphere0];
+  if (cc.n_planes > 0) c.p0 = a.planes[cc.plane0];
+  return c;
+}
+
+// Colliders and/or the contact mask: the lane's 4 nodes together, each node through the same
+// IEEE round-to-nearest sequence as advance_with_impulse (sc_device.cuh: plug_tail, the
+// velocity-level response on the old positions, x' = x + v' dt, the position-level projection,
+// the re-pin), so contact decisions and masks match PARITY. The x and y components run as
+// packed f32x2 RN operations (__fadd2_rn / __fmul2_rn: per-lane IEEE results, never
+// contracted), which gives the same bits as the scalar sequence at half the instructions.
 __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const ClothConst<float>& cc,
-                                               int b, int k, int Rf, int ix0, float t_next,
-                                               const float2 (&P0)[4], const float2 (&Z0)[2],
-                                               const float2 (&xs)[4], const float2 (&vs)[4],
-                                               const float (&xz)[4], const float (&vz)[4],
-                                               float (&xo)[4][3], float (&vo)[4][3],
-                                               uint8_t (&mk)[4]) {
+                                               const Colliders& col, int b, int k, int Rf,
+                                               int ix0, float t_next, const float2 (&P0)[4],
+                                               const float2 (&Z0)[2], const float2 (&xs)[4],
+                                               const float2 (&vs)[4], const float (&xz)[4],
+                                               const float (&vz)[4], float (&xo)[4][3],
+                                               float (&vo)[4][3], uint8_t (&mk)[4]) {
   const int nx = a.nx;
-  float x[4][3];
-  bool fin_imp = true;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float v[3] = {vs[q].x, vs[q].y, vz[q]};
-    float imp[3] = {P0[q].x, P0[q].y, zc(Z0, q)};
-    fin_imp = fin_imp && isfinite(imp[0]) && isfinite(imp[1]) && isfinite(imp[2]);
-    plug_tail(cc, v, imp);
-    x[q][0] = xs[q].x;
-    x[q][1] = xs[q].y;
-    x[q][2] = xz[q];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) vo[q][d] = __fadd_rn(v[d], imp[d]);
-    mk[q] = 0;
-  }
-  if (a.health && !fin_imp) {
+  if (a.health) {  // non-finite cell impulse: first (step, node) (net.cpp:139-140)
     for (int q = 0; q < 4; ++q)
       if (!(isfinite(P0[q].x) && isfinite(P0[q].y) && isfinite(zc(Z0, q)))) {
         const unsigned long long key = (static_cast<unsigned long long>(k + 1) << 32) |
@@ -653,33 +655,110 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
         break;
       }
   }
+  // add_plug_impulse tail (kernels.hpp:188-195): gravity, then drag
+  float2 ixy[4];
+  float iz[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    ixy[q] = P0[q];
+    iz[q] = zc(Z0, q);
+  }
+  if (cc.plug_gravity) {
+    const float2 g = make_float2(cc.dv[0], cc.dv[1]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ixy[q] = __fadd2_rn(ixy[q], g);
+      iz[q] = __fadd_rn(iz[q], cc.dv[2]);
+    }
+  }
+  if (cc.plug_drag) {  // imp - v * drag_c (a subtraction is the addition of the exact negation)
+    const float2 d = make_float2(cc.drag_c, cc.drag_c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 m = __fmul2_rn(vs[q], d);
+      ixy[q] = __fadd2_rn(ixy[q], make_float2(-m.x, -m.y));
+      iz[q] = __fsub_rn(iz[q], __fmul_rn(vz[q], cc.drag_c));
+    }
+  }
+  // vv = v + imp
+  float2 vxy[4];
+  float vzz[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    vxy[q] = __fadd2_rn(vs[q], ixy[q]);
+    vzz[q] = __fadd_rn(vz[q], iz[q]);
+    mk[q] = 0;
+  }
+  // velocity-level response on the OLD positions (kernels.hpp:213-225): spheres, then planes
 #pragma unroll 1
   for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<float> sp = a.spheres[cc.sphere0 + s];
+    const SphereConst<float> sp = s == 0 ? col.s0 : a.spheres[cc.sphere0 + s];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sphere_velocity(sp, x[q], vo[q], mk[q]);
+    for (int q = 0; q < 4; ++q) {
+      const float x[3] = {xs[q].x, xs[q].y, xz[q]};
+      float vv[3] = {vxy[q].x, vxy[q].y, vzz[q]};
+      sphere_velocity(sp, x, vv, mk[q]);
+      vxy[q] = make_float2(vv[0], vv[1]);
+      vzz[q] = vv[2];
+    }
   }
 #pragma unroll 1
   for (int s = 0; s < cc.n_planes; ++s) {
-    const PlaneConst<float> pl = a.planes[cc.plane0 + s];
+    const PlaneConst<float> pl = s == 0 ? col.p0 : a.planes[cc.plane0 + s];
+    const float2 omf = make_float2(pl.omf, pl.omf);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) plane_velocity(pl, x[q], vo[q], mk[q]);
+    for (int q = 0; q < 4; ++q) {  // plane_velocity, branch-free (selects, no divergence)
+      const bool c = __fsub_rn(xz[q], pl.h) <= pl.band && vzz[q] < 0.f;
+      const float2 d = __fmul2_rn(vxy[q], omf);
+      const float dz = __fmul_rn(__fsub_rn(vzz[q], vzz[q]), pl.omf);
+      vxy[q] = c ? d : vxy[q];
+      vzz[q] = c ? dz : vzz[q];
+      mk[q] = c ? 1 : mk[q];
+    }
+  }
+  // x' = x + vv dt (kernels.hpp:226-227)
+  float2 pxy[4];
+  float pz[4];
+  {
+    const float2 dt2 = make_float2(cc.dt, cc.dt);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      pxy[q] = __fadd2_rn(xs[q], __fmul2_rn(vxy[q], dt2));
+      pz[q] = __fadd_rn(xz[q], __fmul_rn(vzz[q], cc.dt));
+    }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) xo[q][d] = __fadd_rn(x[q][d], __fmul_rn(vo[q][d], cc.dt));
+  for (int q = 0; q < 4; ++q) {
+    xo[q][0] = pxy[q].x;
+    xo[q][1] = pxy[q].y;
+    xo[q][2] = pz[q];
+    vo[q][0] = vxy[q].x;
+    vo[q][1] = vxy[q].y;
+    vo[q][2] = vzz[q];
+  }
+  // position-level intersection elimination (kernels.hpp:229-244): spheres, then planes
 #pragma unroll 1
   for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<float> sp = a.spheres[cc.sphere0 + s];
+    const SphereConst<float> sp = s == 0 ? col.s0 : a.spheres[cc.sphere0 + s];
 #pragma unroll
     for (int q = 0; q < 4; ++q) sphere_position(sp, xo[q], vo[q], mk[q]);
   }
 #pragma unroll 1
   for (int s = 0; s < cc.n_planes; ++s) {
-    const PlaneConst<float> pl = a.planes[cc.plane0 + s];
+    const PlaneConst<float> pl = s == 0 ? col.p0 : a.planes[cc.plane0 + s];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) plane_position(pl, xo[q], vo[q], mk[q]);
+    for (int q = 0; q < 4; ++q) {  // plane_position, branch-free
+      const bool below = xo[q][2] < pl.h;
+      const float vn = vo[q][2];
+      const bool damp = below && vn < 0.f;
+      const float dx = __fmul_rn(vo[q][0], pl.omf), dy = __fmul_rn(vo[q][1], pl.omf);
+      const float dz = __fmul_rn(__fsub_rn(vo[q][2], vn), pl.omf);
+      xo[q][2] = below ? pl.h : xo[q][2];
+      vo[q][0] = damp ? dx : vo[q][0];
+      vo[q][1] = damp ? dy : vo[q][1];
+      vo[q][2] = damp ? dz : vo[q][2];
+      mk[q] = below ? 1 : mk[q];
+    }
   }
   if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
 #pragma unroll

@@ -152,6 +152,7 @@ struct StepArgs {
   int32_t u0, u1;        // global rows to update [u0, u1)
   int32_t batch;
   int32_t b_off;         // FAST launches over cloths [b_off, b_off + batch) (pipelined rollout)
+  const int32_t* ids;    // FAST launches: cloth b of the launch is ids[b] (class groups), or b
   int32_t zs;            // z planes carry the z_col swizzle (contexts on the general finish)
   int32_t k;             // step index: t_next = T(k+1) * dt
   int32_t use_t_override;

@@ -68,12 +68,15 @@ struct WavePlan {
   int rev;        // level order reversed across warp slots (issue priority to deep levels)
   uint32_t hint_ns;  // mbarrier try_wait suspend-time hint (0: the hardware default)
 };
-WavePlan plan_wave(int nx, int ny, int batch, int device, bool general);
+// max_ctas > 0: use at most that many SMs (the rest stay free for a concurrent launch)
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas = 0);
 size_t wave_smem_bytes(int levels, int slots);
-// `steps` timesteps k = a.k .. a.k + steps - 1 of every cloth, in place in a.out (== a.in);
-// tmap: the tensor maps of that buffer.
+// `steps` timesteps k = a.k .. a.k + steps - 1 of the launch's cloths (a.batch of them from
+// a.b_off, through a.ids when set), from a.in (tensor maps tmap) into a.out (tmap_out); a.in ==
+// a.out updates in place.
 cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
-                        const WavePlan& plan, int steps, cudaStream_t stream);
+                        const CUtensorMap* tmap_out, const WavePlan& plan, int steps,
+                        cudaStream_t stream);
 
 // layout.cu: AoS [batch][node][3] <-> planar [batch][6][rows][pitch]
 // (rows = the ctx's local rows; AoS arrays hold exactly those rows.)

@@ -46,14 +46,27 @@ constexpr int kWavePrefetch = 4;  // row positions the loader runs ahead of warp
 __device__ __forceinline__ void bar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// A wait that never hangs the device: after 20 s without the phase completing (a protocol bug,
+// never a legitimate wait) the kernel traps, so the host sees a launch error instead of a hung
+// GPU. The timer is read only on the retry path.
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
   if (hint_ns) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
+        ".reg .u64 t0, t1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@p bra DONE_%=;\n"
+        "mov.u64 t0, %%globaltimer;\n"
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAIT_%=;\n"
+        "@p bra DONE_%=;\n"
+        "mov.u64 t1, %%globaltimer;\n"
+        "sub.u64 t1, t1, t0;\n"
+        "setp.gt.u64 p, t1, 20000000000;\n"
+        "@p trap;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
         "}\n" ::"r"(bar),
         "r"(parity), "r"(hint_ns)
         : "memory");
@@ -61,9 +74,19 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity, uint32_t
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
+        ".reg .u64 t0, t1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "mov.u64 t0, %%globaltimer;\n"
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
+        "@p bra DONE_%=;\n"
+        "mov.u64 t1, %%globaltimer;\n"
+        "sub.u64 t1, t1, t0;\n"
+        "setp.gt.u64 p, t1, 20000000000;\n"
+        "@p trap;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
         "}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
@@ -83,6 +106,7 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 template <bool ALPHA1, int W, bool GEN, bool ZS>
 __global__ void __launch_bounds__(32 * W, 1)
     wave_kernel(const __grid_constant__ CUtensorMap tmap_xy, const __grid_constant__ CUtensorMap tmap_z,
+                const __grid_constant__ CUtensorMap tout_xy, const __grid_constant__ CUtensorMap tout_z,
                 const StepArgs<float> a, const FastNet f, const int steps, const int slots,
                 const int rev, const uint32_t hint) {
   extern __shared__ __align__(128) float ring[];
@@ -113,22 +137,26 @@ __global__ void __launch_bounds__(32 * W, 1)
   // c0 + i % m) row R at position 2 + i L + R
   const int Q = 2 + passes * m * L;
 
-  // ---- loader state (warp 0): its own cursor over (item, row) ----
-  int ld_q = 0, ld_R = ny, ld_c = c0, ld_ci = 0;  // positions 0, 1: rows ny, ny+1 (OOB: zeros)
-  int ld_s = 0;
-  uint32_t ld_cyc = 0;  // ring cycle of position ld_q (its slot's barrier phases are ld_cyc & 1)
   const uint32_t ring_s = opaque(smem_u32(ring)), full_s = opaque(smem_u32(full));
   const uint32_t free_s = opaque(smem_u32(freeb)), lev_s = opaque(smem_u32(lev));
   // level of this warp: warp w runs timestep w of every pass (rev: timestep W-1-w, so the
   // hardware's issue priority of low warp slots goes to the deep levels)
   const int lvl = rev ? W - 1 - warp : warp;
-  auto issue_next = [&]() {
-    if (ld_q >= Q) return;
-    if (ld_q >= slots)  // the slot's previous position (cycle ld_cyc - 1) must be released
-      bar_wait(free_s + 8u * static_cast<uint32_t>(ld_s), (ld_cyc - 1u) & 1u, hint);
-    const uint32_t dst = ring_s + static_cast<uint32_t>(ld_s) * (ROWF * 4);
-    const uint32_t bar = full_s + static_cast<uint32_t>(ld_s) * 8;
-    const int crow = ld_R, cb = ld_c;
+
+  // Loader (level 0): row `crow` of cloth `cb` into slot `slot` (ring cycle `cyc_t`); rows past
+  // the cloth (the two tail rows, and the two rows in front of the first cloth) come out of
+  // bounds and are zero-filled by TMA. Stateless: warp 0 derives each target from its own
+  // position, so the other warps carry no loader registers.
+  // pass 0 reads a.in (tmap_*), later passes what the previous pass stored in a.out (tout_*);
+  // a.in == a.out updates in place
+  auto issue = [&](int ci_t, int crow, int slot, uint32_t cyc_t, bool first_pass) {
+    const int cb = a.ids ? __ldg(a.ids + c0 + ci_t) : c0 + ci_t;
+    const CUtensorMap* mxy = first_pass ? &tmap_xy : &tout_xy;
+    const CUtensorMap* mz = first_pass ? &tmap_z : &tout_z;
+    if (cyc_t > 0)  // the slot's previous position (cycle cyc_t - 1) must be released
+      bar_wait(free_s + 8u * static_cast<uint32_t>(slot), (cyc_t - 1u) & 1u, hint);
+    const uint32_t dst = ring_s + static_cast<uint32_t>(slot) * (ROWF * 4);
+    const uint32_t bar = full_s + static_cast<uint32_t>(slot) * 8;
     if (elect_one()) {
       // the row was last written by generic stores (HBM: the previous pass's last level; smem:
       // the levels of the slot's previous row): order them before the async-proxy copy
@@ -140,29 +168,13 @@ __global__ void __launch_bounds__(32 * W, 1)
       asm volatile(
           "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-          "l"(reinterpret_cast<uint64_t>(&tmap_xy)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
+          "l"(reinterpret_cast<uint64_t>(mxy)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
           : "memory");
       asm volatile(
           "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + Z_X * 4),
-          "l"(reinterpret_cast<uint64_t>(&tmap_z)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
+          "l"(reinterpret_cast<uint64_t>(mz)), "r"(-4), "r"(crow), "r"(0), "r"(cb), "r"(bar)
           : "memory");
-    }
-    // advance the cursor
-    ++ld_q;
-    if (++ld_s == slots) {
-      ld_s = 0;
-      ++ld_cyc;
-    }
-    if (++ld_R == L) {
-      ld_R = 0;
-      if (++ld_ci == m) ld_ci = 0;
-      ld_c = c0 + ld_ci;
-    }
-    if (ld_q == 2) {  // the first real item starts at row 0 of the first cloth
-      ld_R = 0;
-      ld_ci = 0;
-      ld_c = c0;
     }
   };
 
@@ -172,8 +184,11 @@ __global__ void __launch_bounds__(32 * W, 1)
   // the position's ring cycle (a waiter never runs a whole cycle ahead of its producer: the ring
   // bounds the distance between levels).
   if (lvl == 0) {
-    for (int d = 0; d < kWavePrefetch; ++d) issue_next();
-    // positions 0 and 1 (the zero rows read as rows -2, -1 of the first cloth)
+    // positions 0, 1: zero rows (read as rows -2, -1 of the first cloth); 2 .. 2 + D - 1: item
+    // 0's first D rows (D <= L: a pass has at least 4 positions); the main loop then keeps the
+    // loader D positions ahead of warp 0
+    for (int d = 0; d < 2 + kWavePrefetch; ++d)
+      issue(0, d < 2 ? ny + d : d - 2, d % slots, static_cast<uint32_t>(d / slots), true);
     bar_wait(full_s, 0, hint);
     bar_wait(full_s + 8, 0, hint);
   }
@@ -188,7 +203,6 @@ __global__ void __launch_bounds__(32 * W, 1)
   const uint32_t lev_wait = lev_s + 8u * static_cast<uint32_t>((lvl > 0 ? lvl - 1 : 0) * slots);
   const uint32_t lev_mine = lev_s + 8u * static_cast<uint32_t>(lvl * slots);
 
-  int q = 2;
   int sl = 2 % slots, s1 = 1, s2 = 0;  // slots of positions q, q-1, q-2
   uint32_t cyc = 0;                     // ring cycle of position q
 #pragma unroll 1
@@ -199,8 +213,9 @@ __global__ void __launch_bounds__(32 * W, 1)
     const int k = a.k + p * W + lvl;  // this warp's step index in this pass
 #pragma unroll 1
     for (int ci = 0; ci < m; ++ci) {
-      const int b = c0 + ci;
+      const int b = a.ids ? __ldg(a.ids + c0 + ci) : c0 + ci;
       const ClothConst<float> cc = a.cloths[b];
+      const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
       const bool simple = cc.n_spheres == 0 && cc.n_planes == 0;
       const float t_next = __fmul_rn(float(k + 1), cc.dt);
       float* const out_b = a.out + static_cast<int64_t>(b) * 6 * S;
@@ -213,7 +228,18 @@ __global__ void __launch_bounds__(32 * W, 1)
 #pragma unroll 1
       for (int R = 0; R < L; ++R) {
         if (lvl == 0) {
-          issue_next();  // position q + kWavePrefetch
+          // position q + kWavePrefetch: row R + D of this cloth, or of the next item
+          int rt = R + kWavePrefetch, ct = ci, pt = p;
+          if (rt >= L) {
+            rt -= L;
+            if (++ct == m) {
+              ct = 0;
+              ++pt;
+            }
+          }
+          const int st = sl + kWavePrefetch;
+          if (pt < passes)
+            issue(ct, rt, st >= slots ? st - slots : st, cyc + (st >= slots ? 1u : 0u), pt == 0);
           bar_wait(full_s + 8u * static_cast<uint32_t>(sl), cyc & 1u, hint);
         } else if (R < ny) {
           // tail rows are zeros the loader wrote (seen through level 0's wait chain); their
@@ -252,7 +278,7 @@ __global__ void __launch_bounds__(32 * W, 1)
             } else {
               float vo[4][3], xo[4][3];
               uint8_t mk[4];
-              finish_general(a, cc, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
+              finish_general(a, cc, col, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
               if (last) {
                 float* gxy = out_b + 2 * (static_cast<int64_t>(Rf) * a.pitch + ix0);
                 float* gz = out_b + 4 * S + static_cast<int64_t>(Rf) * a.pitch + ix0;
@@ -287,7 +313,6 @@ __global__ void __launch_bounds__(32 * W, 1)
           sl = 0;
           ++cyc;
         }
-        ++q;
       }
     }
   }
@@ -323,7 +348,7 @@ size_t wave_smem_bytes(int levels, int slots) {
          sizeof(uint64_t) * static_cast<size_t>(slots) * (2 + (levels - 1));
 }
 
-WavePlan plan_wave(int nx, int ny, int batch, int device, bool general) {
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas) {
   WavePlan p{};
   p.ok = false;
   if (nx > STRIP || ny < 2 || batch < 1) return p;
@@ -331,11 +356,12 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  // W = 12 levels (384 threads, 160 registers: the row pass fits without spilling; 16 levels
-  // spill at 128 registers); 8 when a cloth-pass is too short for 12 sweeps three rows apart
-  int want = 12;
+  // W = 12 levels (384 threads, 160 registers) with the collider finish, whose register peak
+  // spills at 128; 8 when a cloth-pass is too short for the sweeps three rows apart
+  // 16 levels (512 threads at 128 registers) when no cloth takes the collider finish
+  int want = general ? 12 : 16;
   if (const char* env = std::getenv("SC_WAVE_LEVELS")) want = std::atoi(env);
-  p.ctas = std::min(batch, sms);
+  p.ctas = std::min(batch, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   const int m_min = batch / p.ctas;  // cloths of the least-loaded CTA
   int slots = 0;
   for (int levels : {16, 12, 8}) {
@@ -369,7 +395,8 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general) {
 }
 
 cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
-                        const WavePlan& p, int steps, cudaStream_t stream) {
+                        const CUtensorMap* tmap_out, const WavePlan& p, int steps,
+                        cudaStream_t stream) {
   if (steps <= 0 || a.batch <= 0) return cudaSuccess;
   void* fn = pick_wave(p.levels, f.alpha1 != 0, p.general, a.zs != 0);
   cudaLaunchConfig_t cfg{};
@@ -382,6 +409,7 @@ cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtens
   int rev = p.rev;
   uint32_t hint = p.hint_ns;
   void* args[] = {const_cast<CUtensorMap*>(&tmap[0]), const_cast<CUtensorMap*>(&tmap[1]),
+                  const_cast<CUtensorMap*>(&tmap_out[0]), const_cast<CUtensorMap*>(&tmap_out[1]),
                   const_cast<StepArgs<float>*>(&a), const_cast<FastNet*>(&f),
                   const_cast<int*>(&steps), const_cast<int*>(&slots), &rev, &hint};
   return cudaLaunchKernelExC(&cfg, fn, args);

@@ -78,14 +78,16 @@ def test_chunked_stepping_vs_oracle(oracle):
     assert okx and okv, "rel err x %.3g v %.3g" % (ex, ev)
 
 
-@pytest.mark.parametrize("chunks,batch,steps", [("2", 300, 14), ("4", 600, 25), ("3", 151, 2)])
-def test_wave_pipelined_rollout_bit_identical(monkeypatch, chunks, batch, steps):
+@pytest.mark.parametrize("cfg_id,chunks,batch,steps", [(5, "2", 300, 14), (5, "4", 600, 25),
+                                                     (2, "3", 151, 2), (2, "2", 200, 9)])
+def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch, steps):
     """The wavefront context's host -> host rollout in cloth chunks (capi.cu
-    rollout_wave_pipelined: H2D / step / D2H of different chunks overlapped) against the plain
-    path and the streaming kernel: bit-identical."""
+    rollout_wave_pipelined: H2D / step / D2H of different chunks overlapped; config 5's mixed
+    classes as class groups per chunk) against the plain path and the streaming kernel:
+    bit-identical."""
     from paper_2403_12820_b200 import ClothBatch, configs
     from paper_2403_12820_b200.api import pinned_empty
-    cfg, scenes, p, x, v = configs.build(5, batch=batch, n=128)
+    cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=128)
     xp, vp = pinned_empty(x.shape), pinned_empty(v.shape)
     xp[...] = x
     vp[...] = v
@@ -100,4 +102,8 @@ def test_wave_pipelined_rollout_bit_identical(monkeypatch, chunks, batch, steps)
         xc, vc = cb.rollout(x, v, steps, 3, "fast")
     assert bits_equal(xb, xa) and bits_equal(vb, va)
     assert bits_equal(xc, xa) and bits_equal(vc, va)
-    assert lp == 3 * int(chunks)  # layout in + wavefront + layout out per chunk
+    K = int(chunks)
+    if cfg_id == 5:  # per chunk: layout in + wavefront + `steps` streaming launches + layout out
+        assert lp == K * (3 + steps)
+    else:  # layout in + wavefront + layout out per chunk
+        assert lp == 3 * K

@@ -46,8 +46,9 @@ def test_wave_matches_per_step_launches(cfg_id, n, batch, steps):
     assert bits_equal(xa, xb) and bits_equal(va, vb)
     assert bits_equal(x2, xb) and bits_equal(v2, vb)
     assert lb >= steps
-    if steps >= 2 and la < lb:
+    if steps >= 2 and cfg_id != 5:
         assert la <= 3  # layout in + one wavefront launch + layout out
+    assert la <= lb
 
 
 @pytest.mark.parametrize("levels", ["8", "12", "16"])
@@ -109,3 +110,22 @@ def test_wave_health_matches_streaming():
     xs, vs = states[0]
     good = [b for b in range(160) if b not in (7, 30, 31)]
     assert np.isfinite(xs[good]).all() and np.isfinite(vs[good]).all()
+
+
+def test_wave_class_groups_bit_identical(monkeypatch):
+    """A batch mixing collider-free and collider cloths runs as two class groups (collider-free
+    cloths in the wavefront kernel, plane / sphere cloths in the streaming kernel); grouped,
+    ungrouped (SC_GROUP=0: one wavefront launch with the collider finish) and per-step streaming
+    give the same bits, odd and even step counts."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    cfg, scenes, p, x, v = configs.build(5, batch=301, n=128)
+    out = {}
+    for group, persistent in (("1", True), ("0", True), ("1", False)):
+        monkeypatch.setenv("SC_GROUP", group)
+        with ClothBatch(scenes, p) as cb:
+            cb.set_persistent(persistent)
+            out[(group, persistent)] = [cb.rollout(x, v, s, 2, "fast") for s in (17, 24)]
+    ref = out[("1", False)]
+    for key, res in out.items():
+        for (xa, va), (xb, vb) in zip(res, ref):
+            assert bits_equal(xa, xb) and bits_equal(va, vb), key

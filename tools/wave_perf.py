@@ -19,11 +19,13 @@ def main():
     ap.add_argument("--levels", default="8,12,16")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--n", type=int, default=0, help="shrink / grow the grid to n x n")
     args = ap.parse_args()
     from paper_2403_12820_b200 import ClothBatch, configs
 
     for cid in [int(c) for c in args.configs.split(",")]:
-        cfg, scenes, p, x, v = configs.build(cid, batch=args.batch or None, threads=16)
+        cfg, scenes, p, x, v = configs.build(cid, batch=args.batch or None, threads=16,
+                                             n=args.n or None)
         steps = args.steps or cfg.steps
         nodes = x.shape[0] * x.shape[1]
         runs = [("stream", None)] + [("wave%s" % l, l) for l in args.levels.split(",")]
