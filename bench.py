@@ -345,11 +345,14 @@ def run_ours(args, world, rank, local):
     mode = args.mode
     peak, peak_src = _peaks()
     extra = {}
-    if cid != 4:
+    if cid != 4 or world == 1:
         # ---- independent cloths: a B/G shard per rank (strong), the whole batch per rank (weak),
         # or replicas of a single-cloth config ----
         if cfg.batch > 1 and args.scaling == "strong":
             b0, b1 = cfg.batch * rank // world, cfg.batch * (rank + 1) // world
+            scaling = "strong"
+        elif cid == 4:  # N = 1: the whole 8192^2 cloth in one context (strips only for N > 1)
+            b0, b1 = 0, 1
             scaling = "strong"
         else:
             b0, b1 = (cfg.batch * rank, cfg.batch * (rank + 1)) if cfg.batch > 1 else (0, 1)
@@ -400,7 +403,8 @@ def run_ours(args, world, rank, local):
                 "l2": "no flush: state %.1f MB per GPU%s" % (
                     24e-6 * nodes_rank, " > 126 MB L2" if 24e-6 * nodes_rank > 126 else
                     " (L2-resident: configs 1/3 are small by definition)"),
-                "parallelism": ("dp%d: %d cloths per GPU, no collective" % (world, B)
+                "parallelism": ("one GPU, whole cloth" if cid == 4 else
+                                "dp%d: %d cloths per GPU, no collective" % (world, B)
                                 if scaling != "replicas" else "replicas only (one cloth)")}
     else:
         # ---- one 8192^2 cloth in row strips, halo rows over NCCL each step ----
