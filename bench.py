@@ -366,9 +366,15 @@ def run_ours(args, world, rank, local):
         cb.sync()
         barrier()
         launches0 = cb.launch_count()
+        nvtx = os.environ.get("SC_BENCH_NVTX") == "1"  # ncu --replay-mode range capture
         with ClockSampler(local) as clocks:
             # CUDA events on the context stream around exactly the K timed timesteps
+            if nvtx:
+                torch.cuda.nvtx.range_push("bench_timed")
             sec = cb.benchmark(K, 0, mode)
+            if nvtx:
+                torch.cuda.synchronize()
+                torch.cuda.nvtx.range_pop()
         launches = cb.launch_count() - launches0
         barrier()
         sec_max = max_over_ranks(sec)
@@ -460,7 +466,9 @@ def run_ours(args, world, rank, local):
     # the timed region on this GPU: algorithmic bytes of all its node-updates over the region's
     # CUDA-event time (launch gaps included); the dominant kernel(s) run the whole region
     achieved = BYTES_PER_NODE_UPDATE * region_nu / sec / 1e9
-    if kernel == "wave_kernel+fast_step_kernel":
+    if kernel == "wave_kernel+fast_step_kernel" and _traffic(kernel, WORKLOAD_KEY[cid], K)[0]:
+        traffic_per_nu, traffic_src = _traffic(kernel, WORKLOAD_KEY[cid], K)  # range capture
+    elif kernel == "wave_kernel+fast_step_kernel":
         tw, src_w = _traffic("wave_kernel", WORKLOAD_KEY[cid], K)
         ts, src_s = _traffic("fast_step_kernel", WORKLOAD_KEY[cid], K)
         traffic_per_nu = ((B - n_coll) * tw + n_coll * ts) / B if tw and ts else None

@@ -49,48 +49,30 @@ __device__ __forceinline__ void bar_arrive(uint32_t bar) {
 // A wait that never hangs the device: after 20 s without the phase completing (a protocol bug,
 // never a legitimate wait) the kernel traps, so the host sees a launch error instead of a hung
 // GPU. The timer is read only on the retry path.
+// hint_ns > 0: a failed try sleeps hint_ns before retrying (a waiting warp then costs almost no
+// issue slots; its SMSP's other warps keep issuing).
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
-  if (hint_ns) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .u64 t0, t1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@p bra DONE_%=;\n"
-        "mov.u64 t0, %%globaltimer;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@p bra DONE_%=;\n"
-        "mov.u64 t1, %%globaltimer;\n"
-        "sub.u64 t1, t1, t0;\n"
-        "setp.gt.u64 p, t1, 20000000000;\n"
-        "@p trap;\n"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n"
-        "}\n" ::"r"(bar),
-        "r"(parity), "r"(hint_ns)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .u64 t0, t1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@p bra DONE_%=;\n"
-        "mov.u64 t0, %%globaltimer;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@p bra DONE_%=;\n"
-        "mov.u64 t1, %%globaltimer;\n"
-        "sub.u64 t1, t1, t0;\n"
-        "setp.gt.u64 p, t1, 20000000000;\n"
-        "@p trap;\n"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-  }
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      ".reg .u64 t0, t1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "mov.u64 t0, %%globaltimer;\n"
+      "WAIT_%=:\n"
+      "setp.ne.u32 p, %2, 0;\n"
+      "@p nanosleep.u32 %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "mov.u64 t1, %%globaltimer;\n"
+      "sub.u64 t1, t1, t0;\n"
+      "setp.gt.u64 p, t1, 20000000000;\n"
+      "@p trap;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
 }
 // an opaque copy: the compiler keeps the value in a register instead of re-deriving it (the
 // shared-window base needs an S2R of the CTA id, which it would otherwise repeat per row)

@@ -1,3 +1,4 @@
-for rev in 0 1; do for hint in 0 1000000 100; do
-  echo "rev=$rev hint=$hint"; SC_WAVE_REV=$rev SC_WAVE_HINT=$hint python tools/wave_perf.py --configs 5 --levels 12 --reps 2 2>&1 | grep wave
-done; done
+# SC_WAVE_HINT sweep (sleep between mbarrier retries) on config 5 and a collider-free batch
+for hint in 0 50 100 200 400 800; do
+  echo "hint=$hint $(SC_WAVE_HINT=$hint timeout 100 python tools/cfg5_class_probe.py mixed simple-only 2>&1 | grep wave | tr '\n' ' ')"
+done
