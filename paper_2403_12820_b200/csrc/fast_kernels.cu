@@ -57,6 +57,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
   const ClothConst<float> cc = a.cloths[b];
   const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
+  const int shape = GEN ? collider_shape(cc) : COLL_ANY;
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
@@ -194,7 +195,14 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
         float vo[4][3], xo[4][3];
         uint8_t mk[4];
-        finish_general(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
+        if (shape == COLL_PLANE1)
+          finish_general<COLL_PLANE1>(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz,
+                                      xo, vo, mk);
+        else if (shape == COLL_SPHERE1)
+          finish_general<COLL_SPHERE1>(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz,
+                                       xo, vo, mk);
+        else
+          finish_general(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo, mk);
         const int sw = (ix0 >> 3) & 2;  // xy_col swizzle of this lane's group
         const float4 xy01 = make_float4(xo[0][0], xo[0][1], xo[1][0], xo[1][1]);
         const float4 xy23 = make_float4(xo[2][0], xo[2][1], xo[3][0], xo[3][1]);

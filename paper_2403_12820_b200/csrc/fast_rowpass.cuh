@@ -638,6 +638,11 @@ __device__ __forceinline__ Colliders load_colliders(const StepArgs<float>& a,
 // the re-pin), so contact decisions and masks match PARITY. The x and y components run as
 // packed f32x2 RN operations (__fadd2_rn / __fmul2_rn: per-lane IEEE results, never
 // contracted), which gives the same bits as the scalar sequence at half the instructions.
+// CS: the cloth's collider set — COLL_ANY (table loops), or the shapes the BASELINE configs use,
+// COLL_PLANE1 (one plane, no sphere: config 5) and COLL_SPHERE1 (one sphere, no plane: config 3),
+// compiled as straight-line code. Same operations in the same order either way.
+constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2;
+template <int CS = COLL_ANY>
 __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const ClothConst<float>& cc,
                                                const Colliders& col, int b, int k, int Rf,
                                                int ix0, float t_next, const float2 (&P0)[4],
@@ -690,9 +695,7 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
     mk[q] = 0;
   }
   // velocity-level response on the OLD positions (kernels.hpp:213-225): spheres, then planes
-#pragma unroll 1
-  for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<float> sp = s == 0 ? col.s0 : a.spheres[cc.sphere0 + s];
+  auto sphere_vel = [&](const SphereConst<float>& sp) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float x[3] = {xs[q].x, xs[q].y, xz[q]};
@@ -701,10 +704,8 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
       vxy[q] = make_float2(vv[0], vv[1]);
       vzz[q] = vv[2];
     }
-  }
-#pragma unroll 1
-  for (int s = 0; s < cc.n_planes; ++s) {
-    const PlaneConst<float> pl = s == 0 ? col.p0 : a.planes[cc.plane0 + s];
+  };
+  auto plane_vel = [&](const PlaneConst<float>& pl) {
     const float2 omf = make_float2(pl.omf, pl.omf);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // plane_velocity, branch-free (selects, no divergence)
@@ -715,6 +716,16 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
       vzz[q] = c ? dz : vzz[q];
       mk[q] = c ? 1 : mk[q];
     }
+  };
+  if constexpr (CS == COLL_SPHERE1) {
+    sphere_vel(col.s0);
+  } else if constexpr (CS == COLL_PLANE1) {
+    plane_vel(col.p0);
+  } else {
+#pragma unroll 1
+    for (int s = 0; s < cc.n_spheres; ++s) sphere_vel(s == 0 ? col.s0 : a.spheres[cc.sphere0 + s]);
+#pragma unroll 1
+    for (int s = 0; s < cc.n_planes; ++s) plane_vel(s == 0 ? col.p0 : a.planes[cc.plane0 + s]);
   }
   // x' = x + vv dt (kernels.hpp:226-227)
   float2 pxy[4];
@@ -737,15 +748,11 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
     vo[q][2] = vzz[q];
   }
   // position-level intersection elimination (kernels.hpp:229-244): spheres, then planes
-#pragma unroll 1
-  for (int s = 0; s < cc.n_spheres; ++s) {
-    const SphereConst<float> sp = s == 0 ? col.s0 : a.spheres[cc.sphere0 + s];
+  auto sphere_pos = [&](const SphereConst<float>& sp) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) sphere_position(sp, xo[q], vo[q], mk[q]);
-  }
-#pragma unroll 1
-  for (int s = 0; s < cc.n_planes; ++s) {
-    const PlaneConst<float> pl = s == 0 ? col.p0 : a.planes[cc.plane0 + s];
+  };
+  auto plane_pos = [&](const PlaneConst<float>& pl) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // plane_position, branch-free
       const bool below = xo[q][2] < pl.h;
@@ -759,6 +766,16 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
       vo[q][2] = damp ? dz : vo[q][2];
       mk[q] = below ? 1 : mk[q];
     }
+  };
+  if constexpr (CS == COLL_SPHERE1) {
+    sphere_pos(col.s0);
+  } else if constexpr (CS == COLL_PLANE1) {
+    plane_pos(col.p0);
+  } else {
+#pragma unroll 1
+    for (int s = 0; s < cc.n_spheres; ++s) sphere_pos(s == 0 ? col.s0 : a.spheres[cc.sphere0 + s]);
+#pragma unroll 1
+    for (int s = 0; s < cc.n_planes; ++s) plane_pos(s == 0 ? col.p0 : a.planes[cc.plane0 + s]);
   }
   if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
 #pragma unroll
@@ -773,6 +790,13 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
       for (int d = 0; d < 3; ++d) fin = fin && isfinite(xo[q][d]) && isfinite(vo[q][d]);
     if (!fin) atomicMin(&a.health[b].state_frame, k + 1);
   }
+}
+
+// finish_general with the collider-set specialisation chosen per cloth (a uniform branch)
+__device__ __forceinline__ int collider_shape(const ClothConst<float>& cc) {
+  return cc.n_spheres == 0 && cc.n_planes == 1   ? COLL_PLANE1
+         : cc.n_spheres == 1 && cc.n_planes == 0 ? COLL_SPHERE1
+                                                 : COLL_ANY;
 }
 
 }  // namespace fastrow
