@@ -39,15 +39,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// try_wait suspend-time hint: a warp whose TMA row has not landed sleeps (NANOSLEEP.SYNCS, woken
+// by the barrier) instead of spinning on issue slots its SM's other warps could use
+constexpr uint32_t kSuspendHintNs = 1000000;
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(kSuspendHintNs)
       : "memory");
 }
 
