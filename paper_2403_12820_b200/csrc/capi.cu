@@ -838,18 +838,57 @@ bool pinned(const void* p) {
 // steps the chunks before it, and its D2H on a second copy stream while the chunks after it
 // step. Each chunk is one wavefront launch over all SMs (chunks of >= 4 cloths per CTA keep
 // its load balance), so the device time is the unchunked one plus one chunk's copies.
+// Cloth-chunk boundaries of the pipelined wavefront rollout. The pipeline is compute-bound when
+// a cloth's `steps` timesteps take longer on the GPU than its upload (per node: ~9e-12 s per
+// node-update at ~1.1e11 node-updates/s against 24 B at ~54 GB/s = 4.4e-10 s each way), i.e. by
+// the factor g = 0.02 steps (6 for config 5's 300 steps). The exposed time is then the first
+// chunk's upload and the last chunk's download, so the chunks ramp geometrically: one wavefront
+// CTA's worth of cloths per SM first, each next chunk at most g x larger (its upload hides behind
+// the previous chunk's stepping), the same ramp mirrored at the end (each download hides behind
+// the next chunk's stepping), the rest in the middle. Chunk sizes are multiples of the SM count
+// where possible (the wavefront grid's load balance). Short rollouts (g < 2) keep K equal chunks.
+std::vector<int> pipeline_bounds(int batch, int sms, int steps, int K_equal) {
+  std::vector<int> b0{0};
+  const double g = 0.8 * 0.0207 * steps;
+  if (g >= 2.0 && batch >= 4 * sms) {
+    std::vector<int> ramp;
+    int64_t size = sms, used = 0;
+    while (2 * (used + size) <= batch - sms) {  // leave at least one SM-wave for the middle
+      ramp.push_back(static_cast<int>(size));
+      used += size;
+      size = static_cast<int64_t>(size * g) / sms * sms;
+      if (size < sms) size = sms;
+    }
+    const int middle = static_cast<int>(batch - 2 * used);
+    std::vector<int> sizes(ramp.begin(), ramp.end());
+    sizes.push_back(middle);
+    sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
+    for (int sz : sizes) b0.push_back(b0.back() + sz);
+    return b0;
+  }
+  for (int i = 1; i <= K_equal; ++i)
+    b0.push_back(static_cast<int>((static_cast<int64_t>(i) * batch) / K_equal));
+  return b0;
+}
+
 bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int k0,
                             void* xo, void* vo) {
   if (const char* env = std::getenv("SC_PIPELINE"))
     if (std::atoi(env) == 0) return false;
   if (!wave_usable(c) || steps < 2 || !xo || !vo) return false;
   if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
-  int K = c->batch >= 16 * c->wave.ctas ? 4 : c->batch >= 8 * c->wave.ctas ? 2 : 1;
-  if (const char* env = std::getenv("SC_WAVE_CHUNKS")) K = std::atoi(env);  // tuning / tests
-  K = std::min(std::min(K, 4), c->batch);
-  if (K < 2) return false;
-  int b0[5];
-  for (int i = 0; i <= K; ++i) b0[i] = static_cast<int>((static_cast<int64_t>(i) * c->batch) / K);
+  int Ke = c->batch >= 16 * c->wave.ctas ? 4 : c->batch >= 8 * c->wave.ctas ? 2 : 1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  std::vector<int> b0;
+  if (const char* env = std::getenv("SC_WAVE_CHUNKS")) {  // tuning / tests: K equal chunks
+    const int K = std::min(std::max(1, std::atoi(env)), c->batch);
+    for (int i = 0; i <= K; ++i) b0.push_back(static_cast<int>((static_cast<int64_t>(i) * c->batch) / K));
+  } else {
+    b0 = pipeline_bounds(c->batch, sms, steps, std::min(Ke, c->batch));
+  }
+  const int K = static_cast<int>(b0.size()) - 1;
+  if (K < 2 || K > 6) return false;  // event slots: ev_in [0, K), ev_out [8, 8 + K), 14-16 taken
   // class-grouped contexts: each chunk's collider-free / collider cloths are contiguous slices
   // of the two (ascending) id lists
   std::vector<int> s_lo(K + 1, 0), g_lo(K + 1, 0);

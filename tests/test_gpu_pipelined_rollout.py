@@ -79,19 +79,24 @@ def test_chunked_stepping_vs_oracle(oracle):
 
 
 @pytest.mark.parametrize("cfg_id,chunks,batch,steps", [(5, "2", 300, 14), (5, "4", 600, 25),
-                                                     (2, "3", 151, 2), (2, "2", 200, 9)])
+                                                     (2, "3", 151, 2), (2, "2", 200, 9),
+                                                     (5, "ramp", 600, 130)])
 def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch, steps):
     """The wavefront context's host -> host rollout in cloth chunks (capi.cu
     rollout_wave_pipelined: H2D / step / D2H of different chunks overlapped; config 5's mixed
     classes as class groups per chunk) against the plain path and the streaming kernel:
-    bit-identical."""
+    bit-identical. "ramp": the default long-rollout chunking (capi.cu pipeline_bounds: chunks of
+    148, 304, 148 cloths for 600 cloths x 130 steps on 148 SMs)."""
     from paper_2403_12820_b200 import ClothBatch, configs
     from paper_2403_12820_b200.api import pinned_empty
     cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=128)
     xp, vp = pinned_empty(x.shape), pinned_empty(v.shape)
     xp[...] = x
     vp[...] = v
-    monkeypatch.setenv("SC_WAVE_CHUNKS", chunks)
+    if chunks != "ramp":
+        monkeypatch.setenv("SC_WAVE_CHUNKS", chunks)
+    else:
+        monkeypatch.delenv("SC_WAVE_CHUNKS", raising=False)
     with ClothBatch(scenes, p) as cb:
         xa, va = cb.rollout(x, v, steps, 3, "fast")  # pageable: one wavefront launch
         l0 = cb.launch_count()
@@ -102,7 +107,7 @@ def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch
         xc, vc = cb.rollout(x, v, steps, 3, "fast")
     assert bits_equal(xb, xa) and bits_equal(vb, va)
     assert bits_equal(xc, xa) and bits_equal(vc, va)
-    K = int(chunks)
+    K = 3 if chunks == "ramp" else int(chunks)
     if cfg_id == 5:  # per chunk: layout in + wavefront + `steps` streaming launches + layout out
         assert lp == K * (3 + steps)
     else:  # layout in + wavefront + layout out per chunk
