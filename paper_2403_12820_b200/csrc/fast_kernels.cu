@@ -57,7 +57,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
   const ClothConst<float> cc = a.cloths[b];
   const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-  const int shape = GEN ? collider_shape(cc) : COLL_ANY;
+  const int shape = GEN ? collider_shape(cc, col) : COLL_ANY;
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
@@ -195,7 +195,10 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
         finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
         float vo[4][3], xo[4][3];
         uint8_t mk[4];
-        if (shape == COLL_PLANE1)
+        if (shape == COLL_PLANE1F)
+          finish_plane_f(a, cc, col.p0, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo,
+                         mk);
+        else if (shape == COLL_PLANE1)
           finish_general<COLL_PLANE1>(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz,
                                       xo, vo, mk);
         else if (shape == COLL_SPHERE1)

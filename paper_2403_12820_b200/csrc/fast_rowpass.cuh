@@ -645,7 +645,8 @@ __device__ __forceinline__ Colliders load_colliders(const StepArgs<float>& a,
 // CS: the cloth's collider set — COLL_ANY (table loops), or the shapes the BASELINE configs use,
 // COLL_PLANE1 (one plane, no sphere: config 5) and COLL_SPHERE1 (one sphere, no plane: config 3),
 // compiled as straight-line code. Same operations in the same order either way.
-constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2;
+// COLL_PLANE1F: one frictionless plane and no sphere, finished by finish_plane_f.
+constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2, COLL_PLANE1F = 3;
 template <int CS = COLL_ANY>
 __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const ClothConst<float>& cc,
                                                const Colliders& col, int b, int k, int Rf,
@@ -796,9 +797,77 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
   }
 }
 
+// One frictionless plane (omf = 1 - friction == 1: config 5's free cloths), no sphere. Every
+// contact decision and the mask depend on z alone (plane normal +z), so z keeps the IEEE
+// round-to-nearest chain of advance_with_impulse (kernels.hpp:205-252, the plane following the
+// sphere's ordering; the same decisions as PARITY) while x, y take the simple finish's contracted
+// chain (FAST tolerance) and the velocity factors omf = 1 are identities, left out. 16 instead of
+// ~35 instructions per node.
+__device__ __forceinline__ void finish_plane_f(const StepArgs<float>& a, const ClothConst<float>& cc,
+                                               const PlaneConst<float>& pl, int b, int k, int Rf,
+                                               int ix0, float t_next, const float2 (&P0)[4],
+                                               const float2 (&Z0)[2], const float2 (&xs)[4],
+                                               const float2 (&vs)[4], const float (&xz)[4],
+                                               const float (&vz)[4], float (&xo)[4][3],
+                                               float (&vo)[4][3], uint8_t (&mk)[4]) {
+  const int nx = a.nx;
+  if (a.health) {  // non-finite cell impulse: first (step, node) (net.cpp:139-140)
+    for (int q = 0; q < 4; ++q)
+      if (!(isfinite(P0[q].x) && isfinite(P0[q].y) && isfinite(zc(Z0, q)))) {
+        const unsigned long long key = (static_cast<unsigned long long>(k + 1) << 32) |
+                                       static_cast<unsigned long long>(Rf * nx + ix0 + q);
+        atomicMin(&a.health[b].impulse_key, key);
+        break;
+      }
+  }
+  const float2 dvxy = make_float2(cc.fin[0], cc.fin[1]);
+  const float drag = cc.fin[3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // x, y: plug (gravity, drag), integrate — contracted
+    float2 imp = __fadd2_rn(P0[q], dvxy);
+    imp = __ffma2_rn(vs[q], make_float2(-drag, -drag), imp);
+    const float2 vv = __fadd2_rn(vs[q], imp);
+    const float2 xx = __ffma2_rn(vv, make_float2(cc.dt, cc.dt), xs[q]);
+    // z: add_plug_impulse tail (kernels.hpp:188-195), vv = v + imp, the velocity-level plane
+    // response on the old position, x' = x + vv dt, the position-level projection — IEEE RN
+    float iz = zc(Z0, q);
+    if (cc.plug_gravity) iz = __fadd_rn(iz, cc.dv[2]);
+    if (cc.plug_drag) iz = __fsub_rn(iz, __fmul_rn(vz[q], cc.drag_c));
+    float vzz = __fadd_rn(vz[q], iz);
+    const bool c = __fsub_rn(xz[q], pl.h) <= pl.band && vzz < 0.f;
+    vzz = c ? __fsub_rn(vzz, vzz) : vzz;
+    float pz = __fadd_rn(xz[q], __fmul_rn(vzz, cc.dt));
+    const bool below = pz < pl.h;
+    const bool damp = below && vzz < 0.f;
+    pz = below ? pl.h : pz;
+    vzz = damp ? __fsub_rn(vzz, vzz) : vzz;
+    mk[q] = (c || below) ? 1 : 0;
+    xo[q][0] = xx.x;
+    xo[q][1] = xx.y;
+    xo[q][2] = pz;
+    vo[q][0] = vv.x;
+    vo[q][1] = vv.y;
+    vo[q][2] = vzz;
+  }
+  if (cc.n_pins > 0 && Rf >= cc.pin_row_lo && Rf <= cc.pin_row_hi) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      repin_t(a, cc, Rf, static_cast<int64_t>(Rf) * nx + ix0 + q, t_next, xo[q], vo[q], mk[q]);
+  }
+  if (a.health) {
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) fin = fin && isfinite(xo[q][d]) && isfinite(vo[q][d]);
+    if (!fin) atomicMin(&a.health[b].state_frame, k + 1);
+  }
+}
+
 // finish_general with the collider-set specialisation chosen per cloth (a uniform branch)
-__device__ __forceinline__ int collider_shape(const ClothConst<float>& cc) {
-  return cc.n_spheres == 0 && cc.n_planes == 1   ? COLL_PLANE1
+__device__ __forceinline__ int collider_shape(const ClothConst<float>& cc, const Colliders& col) {
+  return cc.n_spheres == 0 && cc.n_planes == 1   ? (col.p0.omf == 1.0f ? COLL_PLANE1F : COLL_PLANE1)
          : cc.n_spheres == 1 && cc.n_planes == 0 ? COLL_SPHERE1
                                                  : COLL_ANY;
 }

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(32 * W, 1)
       const int b = a.ids ? __ldg(a.ids + c0 + ci) : c0 + ci;
       const ClothConst<float> cc = a.cloths[b];
       const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-      const int shape = GEN ? collider_shape(cc) : COLL_ANY;
+      const int shape = GEN ? collider_shape(cc, col) : COLL_ANY;
       const bool simple = cc.n_spheres == 0 && cc.n_planes == 0;
       const float t_next = __fmul_rn(float(k + 1), cc.dt);
       float* const out_b = a.out + static_cast<int64_t>(b) * 6 * S;
@@ -262,7 +262,10 @@ __global__ void __launch_bounds__(32 * W, 1)
             } else {
               float vo[4][3], xo[4][3];
               uint8_t mk[4];
-              if (shape == COLL_PLANE1)
+              if (shape == COLL_PLANE1F)
+                finish_plane_f(a, cc, col.p0, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo,
+                               vo, mk);
+              else if (shape == COLL_PLANE1)
                 finish_general<COLL_PLANE1>(a, cc, col, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz,
                                             vz, xo, vo, mk);
               else
