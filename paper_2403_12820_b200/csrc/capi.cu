@@ -853,7 +853,9 @@ std::vector<int> pipeline_bounds(int batch, int sms, int steps, int K_equal) {
   if (g >= 2.0 && batch >= 4 * sms) {
     std::vector<int> ramp;
     int64_t size = sms, used = 0;
-    while (2 * (used + size) <= batch - sms) {  // leave at least one SM-wave for the middle
+    // at most two ramp chunks per side (K <= 5: the event slots below), at least one SM-wave of
+    // cloths left for the middle
+    while (ramp.size() < 2 && 2 * (used + size) <= batch - sms) {
       ramp.push_back(static_cast<int>(size));
       used += size;
       size = static_cast<int64_t>(size * g) / sms * sms;
