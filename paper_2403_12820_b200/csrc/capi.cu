@@ -911,8 +911,11 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
       if (c->wave_chunk.find(key) == c->wave_chunk.end())
         c->wave_chunk[key] = plan_wave(c->nx, c->ny, ns, c->device, false, c->wave_simple.ctas);
       if (ns > 0 && !c->wave_chunk[key].ok) return false;
-      if (c->plan_cache.find(-1 - ng) == c->plan_cache.end())
-        c->plan_cache[-1 - ng] = plan_fast(c->nx, c->u1 - c->u0, ng, c->device, false, true);
+      // the collider cloths' streaming launches get the SMs the chunk's wavefront grid leaves
+      const long long gkey = -1 - (static_cast<long long>(ng) << 20) - ns;
+      if (c->plan_cache.find(gkey) == c->plan_cache.end())
+        c->plan_cache[gkey] = plan_fast(c->nx, c->u1 - c->u0, ng, c->device, false, true,
+                                        sms - std::min(ns, c->wave_simple.ctas));
       continue;
     }
     if (c->wave_chunk.find(nb) == c->wave_chunk.end())
@@ -956,7 +959,7 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
     if (c->grouped) {
       const int ns = s_lo[i + 1] - s_lo[i], ng = g_lo[i + 1] - g_lo[i];
       grouped_steps(c, steps, k0, s_lo[i], ns, g_lo[i], ng, c->wave_chunk[-1 - ns],
-                    c->plan_cache[-1 - ng], c->stream);
+                    c->plan_cache[-1 - (static_cast<long long>(ng) << 20) - ns], c->stream);
     } else {
       StepArgs<float> a = base_args<float>(c);
       a.out = st;  // in place
@@ -1187,7 +1190,8 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
                           cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
             ck(cudaMemcpy(c->ids_general.p, general.data(), sizeof(int32_t) * general.size(),
                           cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
-            c->plan_general = plan_fast(c->nx, c->u1 - c->u0, c->n_general, c->device, false, true);
+            c->plan_general = plan_fast(c->nx, c->u1 - c->u0, c->n_general, c->device, false, true,
+                                        sms - c->wave_simple.ctas);
             c->grouped = true;
           }
         }

@@ -465,13 +465,15 @@ size_t fast_smem_bytes(int ring, bool general) {
   return sizeof(float) * (ring * ROWF + (ring == 5 ? 32 * 13 : 0)) + pad;  // pad: tuning knob
 }
 
-FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general) {
+FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general,
+                   int max_sms) {
   FastPlan p{};
   p.ring = pressure ? 5 : 4;
   p.general = general;
   p.n_strips = (nx + STRIP - 1) / STRIP;
   int sms = 148, occ = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (max_sms > 0) sms = std::min(sms, max_sms);
   const size_t smem = fast_smem_bytes(p.ring, general);
   for (void* k : {pick_kernel(true, p.ring), pick_kernel(false, p.ring),
                   p.ring == 5 ? simple_kernel_ptr<true, 5>() : simple_kernel_ptr<true, 4>(),

@@ -47,7 +47,9 @@ struct FastPlan {
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
 bool fast_supported(const NetConst<float>& net, int nx);
-FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general);
+// max_sms > 0: plan the segmentation for that many SMs (the rest run a concurrent launch)
+FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool general,
+                   int max_sms = 0);
 // tmap[0]: xy pairs of a.in as 8-byte elements, dims (pitch, rows, 2, batch), box (136,1,2,1);
 // tmap[1]: z planes, dims (pitch, rows, 2, batch) from element 4S, box (136,1,2,1).
 cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtensorMap* tmap,
