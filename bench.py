@@ -11,7 +11,8 @@ wind, dt = 1/240, 300 timesteps, the reference's 12-channel cell with N(0, 0.05)
 (SURVEY.md §8(d) mapping); it is the largest single-GPU config and the one BASELINE quotes its
 1/2/4/8-GPU sweep on. `--config 2|3|4|1` runs the others. One bench "step" = one timestep of
 the whole batch; the K timed steps run device-resident (config 5: one wavefront launch that
-advances all K timesteps, csrc/wave_kernels.cu).
+advances all K timesteps, csrc/wave_kernels.cu, beside the streaming launches of its plane
+cloths; config 1: one small-cloth launch, csrc/small_kernels.cu).
 
 Multi-GPU (one process per GPU): configs 2 and 5 shard the fixed batch B/G per rank (strong
 scaling, no data-path collective; `--scaling weak` gives every rank the whole batch instead),
@@ -382,7 +383,9 @@ def run_ours(args, world, rank, local):
         if mode != "fast":
             kernel = "parity_kernel"
         elif launches == 1:
-            kernel = "wave_kernel"
+            # one launch for all K timesteps: the small-cloth kernel (<= 1024 nodes per cloth,
+            # csrc/small_kernels.cu) or the wavefront kernel (nx <= 128, csrc/wave_kernels.cu)
+            kernel = "small_kernel" if cfg.n * cfg.n <= 1024 else "wave_kernel"
         elif launches == K + 1 and 0 < n_coll < B:
             kernel = "wave_kernel+fast_step_kernel"  # class groups, concurrent (capi.cu)
         else:

@@ -153,10 +153,13 @@ sc_status sc_ctx_get_health(sc_ctx* ctx, int32_t* first_bad_impulse_frame,
 sc_status sc_ctx_set_health_checks(sc_ctx* ctx, int32_t on);
 /* FAST mode runs multi-step advances of narrow-cloth batches (nx <= 128, no pressure plug) as
  * one persistent wavefront launch: W timesteps per pass over HBM, rows updated in place in
- * shared memory (wave_kernels.cu), bit-identical to one launch per step. Off: one streaming
- * launch per step (programmatic dependent launch chains them). Default on; the environment
- * variable SC_WAVE=0 turns it off for contexts that never called this. Mask-producing last steps
- * and contexts outside the kernel's domain always take the streaming kernel. */
+ * shared memory (wave_kernels.cu), bit-identical to one launch per step; cloths of at most 1024
+ * nodes as one small-cloth launch (one thread per node, the state in shared memory,
+ * small_kernels.cu; within the FAST tolerance; SC_SMALL=0 turns that one off). Off: one
+ * streaming launch per step (programmatic dependent launch chains them). Default on; the
+ * environment variable SC_WAVE=0 turns it off for contexts that never called this.
+ * Mask-producing last steps and contexts outside the kernels' domains always take the streaming
+ * kernel. */
 sc_status sc_ctx_set_persistent(sc_ctx* ctx, int32_t on);
 
 /* Host-to-host rollout: upload x0/v0, advance `steps`, download the final state. When

@@ -80,6 +80,14 @@ cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtens
                         const CUtensorMap* tmap_out, const WavePlan& plan, int steps,
                         cudaStream_t stream);
 
+// small_kernels.cu: cloths of at most 1024 nodes (config 1): one CTA per cloth, one thread per
+// node, the state double-buffered in shared memory, all `steps` timesteps of a.k .. in one launch
+// from a.in into a.out. Per-node cell evaluation in the reference's channel order (FAST
+// arithmetic; within the FAST tolerance, not bit-identical to the row-pass kernels).
+bool small_supported(int nx, int ny);
+cudaError_t launch_small(const StepArgs<float>& a, const FastNet& f, bool general, int steps,
+                         cudaStream_t stream);
+
 // layout.cu: AoS [batch][node][3] <-> planar [batch][6][rows][pitch]
 // (rows = the ctx's local rows; AoS arrays hold exactly those rows.)
 template <typename T>

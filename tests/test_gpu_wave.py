@@ -27,8 +27,9 @@ CASES = [
 
 
 @pytest.mark.parametrize("cfg_id,n,batch,steps", CASES)
-def test_wave_matches_per_step_launches(cfg_id, n, batch, steps):
+def test_wave_matches_per_step_launches(monkeypatch, cfg_id, n, batch, steps):
     from paper_2403_12820_b200 import ClothBatch, configs
+    monkeypatch.setenv("SC_SMALL", "0")  # config 1's 32^2 cloth: the wavefront kernel, not small
     cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=n)
     with ClothBatch(scenes, p) as cb:
         cb.set_persistent(True)
