@@ -18,18 +18,13 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "fast_rowpass.cuh"
-#include "sc_device.cuh"
-#include "sc_kernels.h"
+#include "node_cell.cuh"
 
 namespace scb {
 
 namespace {
 
 constexpr int kSmallMaxNodes = 1024;
-// canonical channel order E,N,W,S,NE,NW,SW,SE,E2,N2,W2,S2 (grid.cpp:14-30)
-__constant__ int kSmallDx[kChannels] = {1, 0, -1, 0, 1, -1, -1, 1, 2, 0, -2, 0};
-__constant__ int kSmallDy[kChannels] = {0, 1, 0, -1, 1, 1, -1, -1, 0, 2, 0, -2};
 
 template <bool ALPHA1, bool GEN>
 __global__ void __launch_bounds__(kSmallMaxNodes, 1)
@@ -54,7 +49,7 @@ __global__ void __launch_bounds__(kSmallMaxNodes, 1)
   int nbr[kChannels];
 #pragma unroll
   for (int c = 0; c < kChannels; ++c) {
-    const int jx = ix + kSmallDx[c], jy = iy + kSmallDy[c];
+    const int jx = ix + nodecell::kDx(c), jy = iy + nodecell::kDy(c);
     nbr[c] = jy * nx + jx;
     if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) valid |= 1u << c;
   }
@@ -73,59 +68,12 @@ __global__ void __launch_bounds__(kSmallMaxNodes, 1)
       for (int d = 0; d < 3; ++d) {
         x[d] = cur[d * n + i];
         v[d] = cur[(3 + d) * n + i];
-        acc[d] = fmaf(v[d], f.wv, f.b[d]);  // b_L + v wV
       }
-#pragma unroll
-      for (int c = 0; c < kChannels; ++c) {
-        if (!((valid >> c) & 1u)) continue;
-        const int j = nbr[c];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const float dx = x[d] - cur[d * n + j];
-          const float dv = v[d] - cur[(3 + d) * n + j];
-          const float q = ALPHA1 ? fmaf(dx, dx, 1.0f) : fmaf(dx * f.alpha[c], dx, 1.0f);
-          const float r = fastrow::rsqrt_q(q);
-          const float w = fmaf(r, fmaf(dv, f.wd[c], f.wn[c]), f.wl[c]);
-          acc[d] = fmaf(dx, w, acc[d]);
-        }
-      }
-      if (a.health) {  // non-finite cell impulse: first (step, node) (net.cpp:139-140)
-        if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
-          const unsigned long long key = (static_cast<unsigned long long>(k + 1) << 32) |
-                                         static_cast<unsigned long long>(gnode);
-          atomicMin(&a.health[b].impulse_key, key);
-        }
-      }
+      nodecell::cell<ALPHA1>(f, x, v, valid,
+                             [&](int c, int d) { return cur[d * n + nbr[c]]; }, acc);
       float xo[3], vo[3];
-      uint8_t mk = 0;
-      if (!GEN || simple) {
-        // plug gravity / drag and integrate, contracted (the simple finish of fast_rowpass.cuh)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const float imp = fmaf(v[d], -cc.fin[3], acc[d] + cc.fin[d]);
-          vo[d] = v[d] + imp;
-          xo[d] = fmaf(vo[d], cc.dt, x[d]);
-        }
-      } else {
-        // plug tail, then advance_with_impulse in IEEE round-to-nearest operations
-        plug_tail(cc, v, acc);
-        float vv[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) vv[d] = __fadd_rn(v[d], acc[d]);
-        for (int q = 0; q < cc.n_spheres; ++q) sphere_velocity(a.spheres[cc.sphere0 + q], x, vv, mk);
-        for (int q = 0; q < cc.n_planes; ++q) plane_velocity(a.planes[cc.plane0 + q], x, vv, mk);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          vo[d] = vv[d];
-          xo[d] = __fadd_rn(x[d], __fmul_rn(vv[d], cc.dt));
-        }
-        for (int q = 0; q < cc.n_spheres; ++q) sphere_position(a.spheres[cc.sphere0 + q], xo, vo, mk);
-        for (int q = 0; q < cc.n_planes; ++q) plane_position(a.planes[cc.plane0 + q], xo, vo, mk);
-      }
-      repin_t(a, cc, iy, gnode, t_next, xo, vo, mk);  // Dirichlet re-pin last
-      if (a.health && !(isfinite(xo[0]) && isfinite(xo[1]) && isfinite(xo[2]) &&
-                        isfinite(vo[0]) && isfinite(vo[1]) && isfinite(vo[2])))
-        atomicMin(&a.health[b].state_frame, k + 1);
+      uint8_t mk;
+      nodecell::finish<GEN>(a, cc, simple, b, k, iy, gnode, t_next, x, v, acc, xo, vo, mk);
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         nxt[d * n + i] = xo[d];
