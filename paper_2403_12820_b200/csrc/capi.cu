@@ -131,6 +131,7 @@ struct sc_ctx {
   FastPlan plan_gen{};   // general finish
   WavePlan wave{};       // wavefront temporal blocking (nx <= 128 batches, no pressure plug)
   bool small_ok = false;  // small-cloth kernel (<= 1024 nodes per cloth, no pressure plug)
+  bool plane_only = false;  // every collider cloth: one frictionless plane, no sphere
   std::map<int, WavePlan> wave_chunk;  // plans for cloth-chunk launches (pipelined rollout)
   // class groups (a batch mixing collider-free cloths with collider cloths): the collider-free
   // ones through the wavefront kernel without the collider finish, the others through the
@@ -680,6 +681,17 @@ bool small_usable(const sc_ctx* c) {
          c->strip_row0 < 0;
 }
 
+// every collider cloth of the scene has exactly one frictionless plane and no sphere
+bool plane_only_scene(const sc_scene_desc* s) {
+  for (int b = 0; b < s->batch; ++b) {
+    const sc_cloth_desc& d = s->cloths[b];
+    if (d.n_spheres > 0 || d.n_planes > 1 ||
+        (d.n_planes == 1 && static_cast<float>(d.planes[0].friction) != 0.0f))
+      return false;
+  }
+  return true;
+}
+
 bool wave_usable(const sc_ctx* c) {
   return c->prec == SC_F32 && c->fast_ok && c->tmap_ok && c->wave.ok && c->wave_on &&
          !c->peer_launch && c->strip_row0 < 0;
@@ -1175,6 +1187,12 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
     // the z-plane swizzle pays on the general-finish FAST kernel only (sc_device.cuh z_col); the
     // state is (re)initialised after set_scene, so the layout is fixed here
     c->zs = c->prec == SC_F32 && c->any_general;
+    // ... except when every collider cloth has one frictionless plane (config 5): their lean
+    // plane finish (finish_plane_f) runs faster on the plain layout — config 5's class-grouped
+    // step 0.598 -> 0.583 ms; one 16-level wavefront launch for every cloth (SC_GROUP=0) 0.593
+    if (c->strip_row0 < 0 && !c->any_pressure && plane_only_scene(s) &&
+        small_supported(c->nx, c->ny) == false && c->nx <= 128)
+      c->zs = false;
     if (const char* env = std::getenv("SC_ZSWIZZLE")) c->zs = c->prec == SC_F32 && std::atoi(env);
     if (c->prec == SC_F32) {
       build_tmaps(c);
@@ -1185,7 +1203,10 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       c->grouped = false;
       c->small_ok = c->strip_row0 < 0 && !c->any_pressure && small_supported(c->nx, c->ny);
       if (c->strip_row0 < 0 && !c->any_pressure) {
-        c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general);
+        // every collider cloth has one frictionless plane and no sphere (config 5)
+        c->plane_only = plane_only_scene(s);
+        if (const char* env = std::getenv("SC_PLANE_ONLY")) c->plane_only = c->plane_only && std::atoi(env);
+        c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general, 0, c->plane_only);
         std::vector<int32_t> simple, general;
         for (int b = 0; b < s->batch; ++b)
           (s->cloths[b].n_spheres > 0 || s->cloths[b].n_planes > 0 ? general : simple).push_back(b);

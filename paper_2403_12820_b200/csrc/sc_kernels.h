@@ -67,11 +67,14 @@ struct WavePlan {
   int ctas;       // persistent CTAs (one per SM, at most one per cloth)
   size_t smem;
   bool general;   // some cloth takes the collider finish
+  int fin;        // finish set compiled in: 0 none, 1 any collider, 2 frictionless planes only
   int rev;        // level order reversed across warp slots (issue priority to deep levels)
   uint32_t hint_ns;  // mbarrier try_wait suspend-time hint (0: the hardware default)
 };
 // max_ctas > 0: use at most that many SMs (the rest stay free for a concurrent launch)
-WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas = 0);
+// plane_only: every collider cloth has one frictionless plane and no sphere (the lean finish)
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas = 0,
+                   bool plane_only = false);
 size_t wave_smem_bytes(int levels, int slots);
 // `steps` timesteps k = a.k .. a.k + steps - 1 of the launch's cloths (a.batch of them from
 // a.b_off, through a.ids when set), from a.in (tensor maps tmap) into a.out (tmap_out); a.in ==

@@ -86,7 +86,10 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 // W warps, one CTA per SM. Dynamic smem: [slots][ROWF] ring, then the barriers
 // full[slots] (TMA landed), freeb[slots] (last level done with the slot),
 // lev[W-1][slots] (level w+1 of the slot's row written back).
-template <bool ALPHA1, int W, bool GEN, bool ZS>
+// FIN: 0 = collider-free cloths only (the collider finish compiled out), 1 = any collider set,
+// 2 = collider cloths with one frictionless plane only (finish_plane_f: a small register peak, so
+// the collider cloths run at 16 levels too)
+template <bool ALPHA1, int W, int FIN, bool ZS>
 __global__ void __launch_bounds__(32 * W, 1)
     wave_kernel(const __grid_constant__ CUtensorMap tmap_xy, const __grid_constant__ CUtensorMap tmap_z,
                 const __grid_constant__ CUtensorMap tout_xy, const __grid_constant__ CUtensorMap tout_z,
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(32 * W, 1)
     for (int ci = 0; ci < m; ++ci) {
       const int b = a.ids ? __ldg(a.ids + c0 + ci) : c0 + ci;
       const ClothConst<float> cc = a.cloths[b];
-      const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-      const int shape = GEN ? collider_shape(cc, col) : COLL_ANY;
+      const Colliders col = FIN ? load_colliders(a, cc) : Colliders{};
+      const int shape = FIN == 1 ? collider_shape(cc, col) : COLL_ANY;
       const bool simple = cc.n_spheres == 0 && cc.n_planes == 0;
       const float t_next = __fmul_rn(float(k + 1), cc.dt);
       float* const out_b = a.out + static_cast<int64_t>(b) * 6 * S;
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(32 * W, 1)
             finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
             // in place (box column of node ix0 is ix0 + 4) or, at the last level, to HBM; the two
             // destinations in separate branches so each store stays in its own address space
-            if (!GEN || simple) {
+            if (!FIN || simple) {
               float xo[3][4], vo[3][4];
               finish_simple(a, cc, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo);
               if (a.health) health_simple(a.health, b, k, Rf, nx, ix0, P0, Z0, xo, vo);
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(32 * W, 1)
             } else {
               float vo[4][3], xo[4][3];
               uint8_t mk[4];
-              if (shape == COLL_PLANE1F)
+              if (FIN == 2 || shape == COLL_PLANE1F)
                 finish_plane_f(a, cc, col.p0, b, k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo,
                                vo, mk);
               else if (shape == COLL_PLANE1)
@@ -311,25 +314,29 @@ __global__ void __launch_bounds__(32 * W, 1)
   // warp 0 drains nothing: every issued load was consumed (the loader stops at Q)
 }
 
-template <bool ALPHA1, int W, bool GEN, bool ZS>
+template <bool ALPHA1, int W, int FIN, bool ZS>
 void* wave_ptr() {
-  return reinterpret_cast<void*>(wave_kernel<ALPHA1, W, GEN, ZS>);
+  return reinterpret_cast<void*>(wave_kernel<ALPHA1, W, FIN, ZS>);
+}
+
+template <int W, int FIN>
+void* pick_wave_f(bool alpha1, bool zs) {
+  return zs ? (alpha1 ? wave_ptr<true, W, FIN, true>() : wave_ptr<false, W, FIN, true>())
+            : (alpha1 ? wave_ptr<true, W, FIN, false>() : wave_ptr<false, W, FIN, false>());
 }
 
 template <int W>
-void* pick_wave_w(bool alpha1, bool gen, bool zs) {
-  if (gen)
-    return zs ? (alpha1 ? wave_ptr<true, W, true, true>() : wave_ptr<false, W, true, true>())
-              : (alpha1 ? wave_ptr<true, W, true, false>() : wave_ptr<false, W, true, false>());
-  return zs ? (alpha1 ? wave_ptr<true, W, false, true>() : wave_ptr<false, W, false, true>())
-            : (alpha1 ? wave_ptr<true, W, false, false>() : wave_ptr<false, W, false, false>());
+void* pick_wave_w(bool alpha1, int fin, bool zs) {
+  return fin == 2 ? pick_wave_f<W, 2>(alpha1, zs)
+         : fin == 1 ? pick_wave_f<W, 1>(alpha1, zs)
+                    : pick_wave_f<W, 0>(alpha1, zs);
 }
 
-void* pick_wave(int levels, bool alpha1, bool gen, bool zs) {
+void* pick_wave(int levels, bool alpha1, int fin, bool zs) {
   switch (levels) {
-    case 8: return pick_wave_w<8>(alpha1, gen, zs);
-    case 12: return pick_wave_w<12>(alpha1, gen, zs);
-    default: return pick_wave_w<16>(alpha1, gen, zs);
+    case 8: return pick_wave_w<8>(alpha1, fin, zs);
+    case 12: return pick_wave_w<12>(alpha1, fin, zs);
+    default: return pick_wave_w<16>(alpha1, fin, zs);
   }
 }
 
@@ -340,7 +347,8 @@ size_t wave_smem_bytes(int levels, int slots) {
          sizeof(uint64_t) * static_cast<size_t>(slots) * (2 + (levels - 1));
 }
 
-WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas) {
+WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_ctas,
+                   bool plane_only) {
   WavePlan p{};
   p.ok = false;
   if (nx > STRIP || ny < 2 || batch < 1) return p;
@@ -351,7 +359,8 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_
   // W = 12 levels (384 threads, 160 registers) with the collider finish, whose register peak
   // spills at 128; 8 when a cloth-pass is too short for the sweeps three rows apart
   // 16 levels (512 threads at 128 registers) when no cloth takes the collider finish
-  int want = general ? 12 : 16;
+  const int fin = general ? (plane_only ? 2 : 1) : 0;
+  int want = fin == 1 ? 12 : 16;
   if (const char* env = std::getenv("SC_WAVE_LEVELS")) want = std::atoi(env);
   p.ctas = std::min(batch, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   const int m_min = batch / p.ctas;  // cloths of the least-loaded CTA
@@ -378,9 +387,10 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_
   if (const char* env = std::getenv("SC_WAVE_HINT")) p.hint_ns = static_cast<uint32_t>(std::atoi(env));
   p.smem = wave_smem_bytes(p.levels, slots);
   p.general = general;
+  p.fin = fin;
   for (bool a1 : {true, false})
     for (bool zs : {true, false})
-      cudaFuncSetAttribute(pick_wave(p.levels, a1, general, zs),
+      cudaFuncSetAttribute(pick_wave(p.levels, a1, fin, zs),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
   p.ok = true;
   return p;
@@ -390,7 +400,7 @@ cudaError_t launch_wave(const StepArgs<float>& a, const FastNet& f, const CUtens
                         const CUtensorMap* tmap_out, const WavePlan& p, int steps,
                         cudaStream_t stream) {
   if (steps <= 0 || a.batch <= 0) return cudaSuccess;
-  void* fn = pick_wave(p.levels, f.alpha1 != 0, p.general, a.zs != 0);
+  void* fn = pick_wave(p.levels, f.alpha1 != 0, p.fin, a.zs != 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(p.ctas));
   cfg.blockDim = dim3(static_cast<unsigned>(32 * p.levels));
