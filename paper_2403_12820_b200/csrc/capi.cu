@@ -681,15 +681,18 @@ bool small_usable(const sc_ctx* c) {
          c->strip_row0 < 0;
 }
 
-// every collider cloth of the scene has exactly one frictionless plane and no sphere
+// some cloth of the scene has a collider, and every such cloth has exactly one frictionless plane
+// and no sphere
 bool plane_only_scene(const sc_scene_desc* s) {
+  bool any = false;
   for (int b = 0; b < s->batch; ++b) {
     const sc_cloth_desc& d = s->cloths[b];
     if (d.n_spheres > 0 || d.n_planes > 1 ||
         (d.n_planes == 1 && static_cast<float>(d.planes[0].friction) != 0.0f))
       return false;
+    any = any || d.n_planes == 1;
   }
-  return true;
+  return any;
 }
 
 bool wave_usable(const sc_ctx* c) {
@@ -949,8 +952,11 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
       // the collider cloths' streaming launches get the SMs the chunk's wavefront grid leaves
       const long long gkey = -1 - (static_cast<long long>(ng) << 20) - ns;
       if (c->plan_cache.find(gkey) == c->plan_cache.end())
+      {
         c->plan_cache[gkey] = plan_fast(c->nx, c->u1 - c->u0, ng, c->device, false, true,
                                         sms - std::min(ns, c->wave_simple.ctas));
+        c->plan_cache[gkey].plane_only = c->plane_only;
+      }
       continue;
     }
     if (c->wave_chunk.find(nb) == c->wave_chunk.end())
@@ -1201,11 +1207,13 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       c->plan_gen = plan_fast(c->nx, c->u1 - c->u0, c->batch, c->device, c->any_pressure, true);
       c->wave = WavePlan{};
       c->grouped = false;
+      c->plane_only = false;
       c->small_ok = c->strip_row0 < 0 && !c->any_pressure && small_supported(c->nx, c->ny);
       if (c->strip_row0 < 0 && !c->any_pressure) {
         // every collider cloth has one frictionless plane and no sphere (config 5)
         c->plane_only = plane_only_scene(s);
         if (const char* env = std::getenv("SC_PLANE_ONLY")) c->plane_only = c->plane_only && std::atoi(env);
+        c->plan.plane_only = c->plan_gen.plane_only = c->plane_only;
         c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general, 0, c->plane_only);
         std::vector<int32_t> simple, general;
         for (int b = 0; b < s->batch; ++b)
@@ -1237,6 +1245,7 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
                           cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
             c->plan_general = plan_fast(c->nx, c->u1 - c->u0, c->n_general, c->device, false, true,
                                         sms - c->wave_simple.ctas);
+            c->plan_general.plane_only = c->plane_only;
             c->grouped = true;
           }
         }

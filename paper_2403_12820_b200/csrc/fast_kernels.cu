@@ -38,8 +38,12 @@ using namespace fastrow;
 // tensor maps and writing a.out. `phase` carries the ring barriers' parity bits across calls
 // (the persistent kernel runs many units / steps on the same ring).
 // GEN = false: no cloth of the launch takes the collider / pressure / mask finish, which is
+// compiled out; PF (with GEN): every collider cloth has one frictionless plane and no pressure
+// plug — the collider finish is finish_plane_f alone (fewer live registers than the general
+// dispatch)
 // then compiled out (fewer live registers around the row loop)
-template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false>
+template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false,
+          bool PF = false>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
                                          const StepArgs<float>& a, const FastNet& f, int b,
                                          int strip, int y0, int y1, float* ring, uint64_t* full,
@@ -57,7 +61,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
   const ClothConst<float> cc = a.cloths[b];
   const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-  const int shape = GEN ? collider_shape(cc, col) : COLL_ANY;
+  const int shape = GEN && !PF ? collider_shape(cc, col) : COLL_ANY;
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
@@ -188,14 +192,14 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           *reinterpret_cast<float4*>(pz) = zgroup<ZS>(ix0, xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
           *reinterpret_cast<float4*>(pz + S2) = zgroup<ZS>(ix0, vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         }
-      } else if (!cc.plug_pressure) {
+      } else if (PF || !cc.plug_pressure) {
         // colliders and/or the contact mask (finish_general), packed stores
         float2 xs[4], vs[4];
         float xz[4], vz[4];
         finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
         float vo[4][3], xo[4][3];
         uint8_t mk[4];
-        if (shape == COLL_PLANE1F)
+        if (PF || shape == COLL_PLANE1F)
           finish_plane_f(a, cc, col.p0, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo,
                          mk);
         else if (shape == COLL_PLANE1)
@@ -354,7 +358,7 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 // segments (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5;
 // MINB 8 = 206 registers is slower again: 631 us).
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB,
-          bool ZS = false>
+          bool ZS = false, bool PF = false>
 __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING, PEER, GEN, ZS>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
+    run_unit<ALPHA1, RING, PEER, GEN, ZS, PF>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
                                  phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
@@ -485,7 +489,9 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
                   p.ring == 5 ? zs_kernel_ptr<false, 5>(true) : zs_kernel_ptr<false, 4>(true),
                   p.ring == 5 ? wide_kernel_ptr<false, 5>() : wide_kernel_ptr<false, 4>(),
                   p.ring == 5 ? peer_kernel_ptr<true, 5>() : peer_kernel_ptr<true, 4>(),
-                  p.ring == 5 ? peer_kernel_ptr<false, 5>() : peer_kernel_ptr<false, 4>()})
+                  p.ring == 5 ? peer_kernel_ptr<false, 5>() : peer_kernel_ptr<false, 4>(),
+                  reinterpret_cast<void*>(fast_step_kernel<true, 4, false, true, SC_FAST_MINB, false, true>),
+                  reinterpret_cast<void*>(fast_step_kernel<false, 4, false, true, SC_FAST_MINB, false, true>)})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
@@ -587,6 +593,15 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
 #define SC_FW(A, R) \
   cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false, kWideMinB>, txy, tz, a, f, ns, sr, ng)
   const bool simple = !peer && !p.general && a.constrained == nullptr && !a.zs;
+  // frictionless planes only, no mask output (a collider-free cloth asked for its mask takes the
+  // general finish)
+  if (!peer && p.general && p.plane_only && !a.zs && p.ring == 4 && a.constrained == nullptr) {
+    return f.alpha1
+               ? cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 4, false, true, SC_FAST_MINB, false, true>,
+                                    txy, tz, a, f, ns, sr, ng)
+               : cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4, false, true, SC_FAST_MINB, false, true>,
+                                    txy, tz, a, f, ns, sr, ng);
+  }
   if (simple && p.wide) {
     if (p.ring == 5) return f.alpha1 ? SC_FW(true, 5) : SC_FW(false, 5);
     return f.alpha1 ? SC_FW(true, 4) : SC_FW(false, 4);

@@ -43,6 +43,7 @@ struct FastPlan {
   bool general;   // some cloth takes the collider / pressure / mask finish
   bool wide;      // simple finish on the wide-register kernel (160 registers, tall segments)
   int occupancy;  // resident CTAs per SM
+  bool plane_only;  // every collider cloth: one frictionless plane, no pressure (lean kernel)
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
