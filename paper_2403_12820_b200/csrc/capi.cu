@@ -132,6 +132,7 @@ struct sc_ctx {
   WavePlan wave{};       // wavefront temporal blocking (nx <= 128 batches, no pressure plug)
   bool small_ok = false;  // small-cloth kernel (<= 1024 nodes per cloth, no pressure plug)
   bool plane_only = false;  // every collider cloth: one frictionless plane, no sphere
+  bool sphere_only = false;  // every collider cloth: one sphere, no plane
   std::map<int, WavePlan> wave_chunk;  // plans for cloth-chunk launches (pipelined rollout)
   // class groups (a batch mixing collider-free cloths with collider cloths): the collider-free
   // ones through the wavefront kernel without the collider finish, the others through the
@@ -681,6 +682,17 @@ bool small_usable(const sc_ctx* c) {
          c->strip_row0 < 0;
 }
 
+// some cloth of the scene has a collider, and every such cloth has exactly one sphere and no plane
+bool sphere_only_scene(const sc_scene_desc* s) {
+  bool any = false;
+  for (int b = 0; b < s->batch; ++b) {
+    const sc_cloth_desc& d = s->cloths[b];
+    if (d.n_planes > 0 || d.n_spheres > 1) return false;
+    any = any || d.n_spheres == 1;
+  }
+  return any;
+}
+
 // some cloth of the scene has a collider, and every such cloth has exactly one frictionless plane
 // and no sphere
 bool plane_only_scene(const sc_scene_desc* s) {
@@ -955,7 +967,7 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
       {
         c->plan_cache[gkey] = plan_fast(c->nx, c->u1 - c->u0, ng, c->device, false, true,
                                         sms - std::min(ns, c->wave_simple.ctas));
-        c->plan_cache[gkey].plane_only = c->plane_only;
+        c->plan_cache[gkey].only = c->plane_only ? 1 : 0;
       }
       continue;
     }
@@ -1193,11 +1205,11 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
     // the z-plane swizzle pays on the general-finish FAST kernel only (sc_device.cuh z_col); the
     // state is (re)initialised after set_scene, so the layout is fixed here
     c->zs = c->prec == SC_F32 && c->any_general;
-    // ... except when every collider cloth has one frictionless plane (config 5): their lean
-    // plane finish (finish_plane_f) runs faster on the plain layout — config 5's class-grouped
-    // step 0.598 -> 0.583 ms; one 16-level wavefront launch for every cloth (SC_GROUP=0) 0.593
-    if (c->strip_row0 < 0 && !c->any_pressure && plane_only_scene(s) &&
-        small_supported(c->nx, c->ny) == false && c->nx <= 128)
+    // ... except when every collider cloth has one collider of one kind — one frictionless plane
+    // (config 5) or one sphere (config 3): the kernels with that finish alone run faster on the
+    // plain layout (config 5's class-grouped step 0.598 -> 0.583 ms with the plane finish; config
+    // 3 22.1 -> 21.7 us with the sphere-only streaming kernel)
+    if (c->strip_row0 < 0 && !c->any_pressure && (plane_only_scene(s) || sphere_only_scene(s)))
       c->zs = false;
     if (const char* env = std::getenv("SC_ZSWIZZLE")) c->zs = c->prec == SC_F32 && std::atoi(env);
     if (c->prec == SC_F32) {
@@ -1208,12 +1220,14 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
       c->wave = WavePlan{};
       c->grouped = false;
       c->plane_only = false;
+      c->sphere_only = false;
       c->small_ok = c->strip_row0 < 0 && !c->any_pressure && small_supported(c->nx, c->ny);
       if (c->strip_row0 < 0 && !c->any_pressure) {
         // every collider cloth has one frictionless plane and no sphere (config 5)
         c->plane_only = plane_only_scene(s);
+        c->sphere_only = sphere_only_scene(s);
         if (const char* env = std::getenv("SC_PLANE_ONLY")) c->plane_only = c->plane_only && std::atoi(env);
-        c->plan.plane_only = c->plan_gen.plane_only = c->plane_only;
+        c->plan.only = c->plan_gen.only = c->plane_only ? 1 : c->sphere_only ? 2 : 0;
         c->wave = plan_wave(c->nx, c->ny, c->batch, c->device, c->any_general, 0, c->plane_only);
         std::vector<int32_t> simple, general;
         for (int b = 0; b < s->batch; ++b)
@@ -1245,7 +1259,7 @@ sc_status sc_ctx_set_scene(sc_ctx* c, const sc_scene_desc* s) {
                           cudaMemcpyHostToDevice), "cudaMemcpy(ids)");
             c->plan_general = plan_fast(c->nx, c->u1 - c->u0, c->n_general, c->device, false, true,
                                         sms - c->wave_simple.ctas);
-            c->plan_general.plane_only = c->plane_only;
+            c->plan_general.only = c->plane_only ? 1 : c->sphere_only ? 2 : 0;
             c->grouped = true;
           }
         }

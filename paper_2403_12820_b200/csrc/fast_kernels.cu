@@ -34,16 +34,19 @@ namespace {
 
 using namespace fastrow;
 
+constexpr int ONLY_PLANE_F = 1, ONLY_SPHERE = 2;
+
 // One unit (cloth b, 128-column strip, rows [y0, y1)) of one step, reading a.in through the
 // tensor maps and writing a.out. `phase` carries the ring barriers' parity bits across calls
 // (the persistent kernel runs many units / steps on the same ring).
 // GEN = false: no cloth of the launch takes the collider / pressure / mask finish, which is
-// compiled out; PF (with GEN): every collider cloth has one frictionless plane and no pressure
-// plug — the collider finish is finish_plane_f alone (fewer live registers than the general
-// dispatch)
+// compiled out; ONLY (with GEN): every collider cloth has one collider of one kind and no
+// pressure plug — the collider finish is that kind's alone (fewer live registers than the
+// general dispatch): ONLY_PLANE_F finish_plane_f (one frictionless plane), ONLY_SPHERE
+// finish_general<COLL_SPHERE1> (one sphere)
 // then compiled out (fewer live registers around the row loop)
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false,
-          bool PF = false>
+          int ONLY = 0>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
                                          const StepArgs<float>& a, const FastNet& f, int b,
                                          int strip, int y0, int y1, float* ring, uint64_t* full,
@@ -61,7 +64,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
   const ClothConst<float> cc = a.cloths[b];
   const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-  const int shape = GEN && !PF ? collider_shape(cc, col) : COLL_ANY;
+  const int shape = GEN && !ONLY ? collider_shape(cc, col) : COLL_ANY;
   const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
                       a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
@@ -192,14 +195,17 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
           *reinterpret_cast<float4*>(pz) = zgroup<ZS>(ix0, xo[2][0], xo[2][1], xo[2][2], xo[2][3]);
           *reinterpret_cast<float4*>(pz + S2) = zgroup<ZS>(ix0, vo[2][0], vo[2][1], vo[2][2], vo[2][3]);
         }
-      } else if (PF || !cc.plug_pressure) {
+      } else if (ONLY || !cc.plug_pressure) {
         // colliders and/or the contact mask (finish_general), packed stores
         float2 xs[4], vs[4];
         float xz[4], vz[4];
         finish_inputs<ZS>(row2, lane, xs, vs, xz, vz);
         float vo[4][3], xo[4][3];
         uint8_t mk[4];
-        if (PF || shape == COLL_PLANE1F)
+        if (ONLY == ONLY_SPHERE)
+          finish_general<COLL_SPHERE1>(a, cc, col, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz,
+                                       xo, vo, mk);
+        else if (ONLY == ONLY_PLANE_F || shape == COLL_PLANE1F)
           finish_plane_f(a, cc, col.p0, b, a.k, Rf, ix0, t_next, P0, Z0, xs, vs, xz, vz, xo, vo,
                          mk);
         else if (shape == COLL_PLANE1)
@@ -358,7 +364,7 @@ __device__ __forceinline__ void decode_unit(int unit, int n_strips, int n_segs, 
 // segments (config 4: 604 -> 571 us/step), but loses on short-segment problems (config 2, 5;
 // MINB 8 = 206 registers is slower again: 631 us).
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, int MINB = SC_FAST_MINB,
-          bool ZS = false, bool PF = false>
+          bool ZS = false, int ONLY = 0>
 __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_constant__ CUtensorMap tmap_xy,
                                                       const __grid_constant__ CUtensorMap tmap_z,
                                                       const StepArgs<float> a, const FastNet f,
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING, PEER, GEN, ZS, PF>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
+    run_unit<ALPHA1, RING, PEER, GEN, ZS, ONLY>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
                                  phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
@@ -460,6 +466,11 @@ void* peer_kernel_ptr() {
 
 
 
+template <bool ALPHA1, bool ZS, int ONLY>
+void* only_kernel_ptr() {
+  return reinterpret_cast<void*>(fast_step_kernel<ALPHA1, 4, false, true, SC_FAST_MINB, ZS, ONLY>);
+}
+
 size_t fast_smem_bytes(int ring, bool general) {
   size_t pad = 0;
   if (const char* env = std::getenv("SC_FAST_SMEM_PAD")) pad = std::strtoul(env, nullptr, 10);
@@ -490,8 +501,10 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
                   p.ring == 5 ? wide_kernel_ptr<false, 5>() : wide_kernel_ptr<false, 4>(),
                   p.ring == 5 ? peer_kernel_ptr<true, 5>() : peer_kernel_ptr<true, 4>(),
                   p.ring == 5 ? peer_kernel_ptr<false, 5>() : peer_kernel_ptr<false, 4>(),
-                  reinterpret_cast<void*>(fast_step_kernel<true, 4, false, true, SC_FAST_MINB, false, true>),
-                  reinterpret_cast<void*>(fast_step_kernel<false, 4, false, true, SC_FAST_MINB, false, true>)})
+                  only_kernel_ptr<true, false, 1>(), only_kernel_ptr<false, false, 1>(),
+                  only_kernel_ptr<true, true, 1>(), only_kernel_ptr<false, true, 1>(),
+                  only_kernel_ptr<true, false, 2>(), only_kernel_ptr<false, false, 2>(),
+                  only_kernel_ptr<true, true, 2>(), only_kernel_ptr<false, true, 2>()})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_kernel(true, p.ring), 32, smem);
   if (occ < 1) occ = 1;
@@ -593,14 +606,18 @@ cudaError_t launch_fast(const StepArgs<float>& a, const FastNet& f, const CUtens
 #define SC_FW(A, R) \
   cudaLaunchKernelEx(&cfg, fast_step_kernel<A, R, false, false, kWideMinB>, txy, tz, a, f, ns, sr, ng)
   const bool simple = !peer && !p.general && a.constrained == nullptr && !a.zs;
-  // frictionless planes only, no mask output (a collider-free cloth asked for its mask takes the
-  // general finish)
-  if (!peer && p.general && p.plane_only && !a.zs && p.ring == 4 && a.constrained == nullptr) {
-    return f.alpha1
-               ? cudaLaunchKernelEx(&cfg, fast_step_kernel<true, 4, false, true, SC_FAST_MINB, false, true>,
-                                    txy, tz, a, f, ns, sr, ng)
-               : cudaLaunchKernelEx(&cfg, fast_step_kernel<false, 4, false, true, SC_FAST_MINB, false, true>,
-                                    txy, tz, a, f, ns, sr, ng);
+  // every collider cloth has one collider of one kind, no mask output (a collider-free cloth
+  // asked for its mask takes the general finish): that kind's finish alone
+  if (!peer && p.general && p.only != 0 && p.ring == 4 && a.constrained == nullptr) {
+#define SC_FO(A, Z, O)                                                                        \
+  cudaLaunchKernelEx(&cfg, fast_step_kernel<A, 4, false, true, SC_FAST_MINB, Z, O>, txy, tz, a, f, \
+                     ns, sr, ng)
+    if (p.only == ONLY_PLANE_F)
+      return a.zs ? (f.alpha1 ? SC_FO(true, true, 1) : SC_FO(false, true, 1))
+                  : (f.alpha1 ? SC_FO(true, false, 1) : SC_FO(false, false, 1));
+    return a.zs ? (f.alpha1 ? SC_FO(true, true, 2) : SC_FO(false, true, 2))
+                : (f.alpha1 ? SC_FO(true, false, 2) : SC_FO(false, false, 2));
+#undef SC_FO
   }
   if (simple && p.wide) {
     if (p.ring == 5) return f.alpha1 ? SC_FW(true, 5) : SC_FW(false, 5);

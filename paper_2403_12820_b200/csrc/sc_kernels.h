@@ -43,7 +43,9 @@ struct FastPlan {
   bool general;   // some cloth takes the collider / pressure / mask finish
   bool wide;      // simple finish on the wide-register kernel (160 registers, tall segments)
   int occupancy;  // resident CTAs per SM
-  bool plane_only;  // every collider cloth: one frictionless plane, no pressure (lean kernel)
+  // every collider cloth: one frictionless plane (1) / one sphere (2), no pressure plug — the
+  // launches without mask output take the kernel with that collider finish alone; 0: dispatch
+  int only;
 };
 FastNet make_fast_net(const NetConst<float>& net);
 // Channel-pair sharing needs gain[c] == gain[negated(c)] (grid.cpp:32-35).
