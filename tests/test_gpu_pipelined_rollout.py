@@ -80,13 +80,13 @@ def test_chunked_stepping_vs_oracle(oracle):
 
 @pytest.mark.parametrize("cfg_id,chunks,batch,steps", [(5, "2", 300, 14), (5, "4", 600, 25),
                                                      (2, "3", 151, 2), (2, "2", 200, 9),
-                                                     (5, "ramp", 600, 130)])
+                                                     (5, "ramp", 600, 200)])
 def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch, steps):
     """The wavefront context's host -> host rollout in cloth chunks (capi.cu
     rollout_wave_pipelined: H2D / step / D2H of different chunks overlapped; config 5's mixed
     classes as class groups per chunk) against the plain path and the streaming kernel:
     bit-identical. "ramp": the default long-rollout chunking (capi.cu pipeline_bounds: chunks of
-    148, 304, 148 cloths for 600 cloths x 130 steps on 148 SMs)."""
+    148, 304, 148 cloths for 600 cloths x 200 steps on 148 SMs)."""
     from paper_2403_12820_b200 import ClothBatch, configs
     from paper_2403_12820_b200.api import pinned_empty
     cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=128)
