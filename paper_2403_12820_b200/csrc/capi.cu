@@ -928,7 +928,8 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
                             void* xo, void* vo) {
   if (const char* env = std::getenv("SC_PIPELINE"))
     if (std::atoi(env) == 0) return false;
-  if (!wave_usable(c) || steps < 2 || !xo || !vo) return false;
+  // small-cloth contexts step in one small-kernel launch on the plain path
+  if (!wave_usable(c) || small_usable(c) || steps < 2 || !xo || !vo) return false;
   if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
   int Ke = c->batch >= 16 * c->wave.ctas ? 4 : c->batch >= 8 * c->wave.ctas ? 2 : 1;
   int sms = 148;
