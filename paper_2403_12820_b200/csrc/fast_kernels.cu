@@ -44,7 +44,6 @@ constexpr int ONLY_PLANE_F = 1, ONLY_SPHERE = 2;
 // pressure plug — the collider finish is that kind's alone (fewer live registers than the
 // general dispatch): ONLY_PLANE_F finish_plane_f (one frictionless plane), ONLY_SPHERE
 // finish_general<COLL_SPHERE1> (one sphere)
-// then compiled out (fewer live registers around the row loop)
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false,
           int ONLY = 0>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
