@@ -723,6 +723,19 @@ int fast_chunks(const sc_ctx* c, int steps) {
   return k;
 }
 
+// The wavefront kernel wins on large narrow-cloth batches; below ~8 cloths per SM its whole
+// cloths per CTA quantise the load (config-5 shares: 512 cloths 82.8 vs 75.1 us per step for
+// the chunked streaming path, 1024: 148.1 vs 145.1; 2048: 290.5 vs 305.8), so smaller batches
+// that can be chunked take the streaming kernel. SC_WAVE_MIN_CLOTHS overrides the threshold.
+bool wave_preferred(const sc_ctx* c, int steps) {
+  if (!wave_usable(c)) return false;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  int min_cloths = 8 * sms;
+  if (const char* env = std::getenv("SC_WAVE_MIN_CLOTHS")) min_cloths = std::atoi(env);
+  return c->batch >= min_cloths || fast_chunks(c, steps) == 0;
+}
+
 template <typename Pre, typename Post>
 void chunked_fast_steps(sc_ctx* c, int K, int steps, int k0, Pre pre, Post post) {
   for (int i = 0; i < K; ++i)
@@ -826,7 +839,7 @@ void advance_impl(sc_ctx* c, int steps, int k0, sc_mode mode, uint8_t* dev_mask_
       steps -= n;
     }
   }
-  if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST && wave_usable(c)) {
+  if (s == 0 && kind == KIND_STEP && mode == SC_MODE_FAST && wave_preferred(c, steps)) {
     const int n = steps - (dev_mask_last ? 1 : 0);  // a mask-producing last step runs whole
     if (n >= 2 && c->grouped) {
       const int out = (c->cur + n) & 1;
@@ -929,7 +942,7 @@ bool rollout_wave_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps
   if (const char* env = std::getenv("SC_PIPELINE"))
     if (std::atoi(env) == 0) return false;
   // small-cloth contexts step in one small-kernel launch on the plain path
-  if (!wave_usable(c) || small_usable(c) || steps < 2 || !xo || !vo) return false;
+  if (!wave_preferred(c, steps) || small_usable(c) || steps < 2 || !xo || !vo) return false;
   if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
   int Ke = c->batch >= 16 * c->wave.ctas ? 4 : c->batch >= 8 * c->wave.ctas ? 2 : 1;
   int sms = 148;
@@ -1053,7 +1066,7 @@ bool rollout_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int
                        void* vo) {
   if (const char* env = std::getenv("SC_PIPELINE"))
     if (std::atoi(env) == 0) return false;
-  if (wave_usable(c)) return false;  // one wavefront launch covers every cloth (TODO overlap)
+  if (wave_preferred(c, steps)) return false;  // the wavefront pipeline (rollout_wave_pipelined)
   const int K = fast_chunks(c, steps);
   if (K == 0 || !xo || !vo) return false;
   if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;

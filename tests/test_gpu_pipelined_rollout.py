@@ -93,6 +93,7 @@ def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch
     xp, vp = pinned_empty(x.shape), pinned_empty(v.shape)
     xp[...] = x
     vp[...] = v
+    monkeypatch.setenv("SC_WAVE_MIN_CLOTHS", "1")  # the wavefront pipeline at these batch sizes
     if chunks != "ramp":
         monkeypatch.setenv("SC_WAVE_CHUNKS", chunks)
     else:

@@ -10,6 +10,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _wave_at_any_batch(monkeypatch):
+    """These tests exercise the wavefront kernel itself: take it whatever the batch size (the
+    default prefers chunked streaming below 8 cloths per SM, capi.cu wave_preferred)."""
+    monkeypatch.setenv("SC_WAVE_MIN_CLOTHS", "1")
+
+
 def bits_equal(a, b):
     a, b = np.asarray(a), np.asarray(b)
     return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
