@@ -144,11 +144,18 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
+# Test hook (never a measurement): SC_BENCH_SHARE_GPU=1 runs every rank on GPU 0 with a gloo
+# process group, so the multi-rank path (batch shares, barriers, max over ranks, rank-0 output)
+# can be exercised on a one-GPU box (tests/test_gpu_bench_ranks.py). Batch-sharded and replica
+# configs only: their ranks never wait on each other's kernels. The line says "shared_gpu".
+SHARE_GPU = os.environ.get("SC_BENCH_SHARE_GPU") == "1"
+
+
 def _spawn(args) -> int:
     """--gpus N without an outer torchrun: launch the N ranks ourselves (same arguments)."""
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not SHARE_GPU:
         print(json.dumps({"error": "bench.py --gpus %d: only %d GPU(s) visible; refusing to "
                           "measure fewer ranks than asked" % (args.gpus, have)}), flush=True)
         return 2
@@ -323,10 +330,18 @@ def run_ours(args, world, rank, local):
 
     from paper_2403_12820_b200 import ClothBatch, configs, strips
 
-    torch.cuda.set_device(local)
+    if SHARE_GPU and args.config == 4 and world > 1:
+        print(json.dumps({"error": "SC_BENCH_SHARE_GPU: config 4's row strips exchange halos "
+                          "over NCCL; not on a shared GPU"}), flush=True)
+        return 2
+    dev = 0 if SHARE_GPU else local
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -336,7 +351,7 @@ def run_ours(args, world, rank, local):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
@@ -361,14 +376,14 @@ def run_ours(args, world, rank, local):
         B = b1 - b0
         _, scenes, params, x, v = configs.build(cid, batch=B, cloth0=b0, threads=16)
         nodes_rank = B * cfg.n * cfg.n
-        cb = ClothBatch(scenes, params, device=local)
+        cb = ClothBatch(scenes, params, device=dev)
         cb.set_state(x, v)
         cb.advance(args.warmup, 0, mode)
         cb.sync()
         barrier()
         launches0 = cb.launch_count()
         nvtx = os.environ.get("SC_BENCH_NVTX") == "1"  # ncu --replay-mode range capture
-        with ClockSampler(local) as clocks:
+        with ClockSampler(dev) as clocks:
             # CUDA events on the context stream around exactly the K timed timesteps
             if nvtx:
                 torch.cuda.nvtx.range_push("bench_timed")
@@ -408,6 +423,8 @@ def run_ours(args, world, rank, local):
         cb.close()
         conf = {"workload": "cfg%d: %s" % (cid, cfg.description), "cloths": cfg.batch,
                 "cloths_per_gpu": B, "grid": "%dx%d" % (cfg.n, cfg.n), "nodes_per_gpu": nodes_rank,
+                **({"shared_gpu": "test hook: every rank on GPU 0 (not a measurement)"}
+                   if SHARE_GPU and world > 1 else {}),
                 "timesteps_per_step": 1, "mode": mode,
                 "l2": "no flush: state %.1f MB per GPU%s" % (
                     24e-6 * nodes_rank, " > 126 MB L2" if 24e-6 * nodes_rank > 126 else
