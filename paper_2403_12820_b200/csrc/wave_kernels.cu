@@ -356,11 +356,13 @@ WavePlan plan_wave(int nx, int ny, int batch, int device, bool general, int max_
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  // W = 12 levels (384 threads, 160 registers) with the collider finish, whose register peak
-  // spills at 128; 8 when a cloth-pass is too short for the sweeps three rows apart
-  // 16 levels (512 threads at 128 registers) when no cloth takes the collider finish
+  // 8 levels when a cloth-pass is too short for the sweeps three rows apart
   const int fin = general ? (plane_only ? 2 : 1) : 0;
-  int want = fin == 1 ? 12 : 16;
+  // 12 levels (384 threads, up to 168 registers): measured faster than 16 for collider-free
+  // batches (config 5's collider-free group 572.5 -> 561.7 us per class-grouped step; a batch of
+  // collider-free cloths alone 570 -> 557) and required by the general collider finish (its
+  // register peak spills at 128); 16 for the lean plane-only finish (605 us per 4096 plane cloths)
+  int want = fin == 2 ? 16 : 12;
   if (const char* env = std::getenv("SC_WAVE_LEVELS")) want = std::atoi(env);
   p.ctas = std::min(batch, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   const int m_min = batch / p.ctas;  // cloths of the least-loaded CTA
