@@ -761,6 +761,7 @@ void chunked_fast_steps(sc_ctx* c, int K, int steps, int k0, Pre pre, Post post)
     a.k = k0 + s;
     for (int i = 0; i < K; ++i) {
       FastPlan p = full;
+      p.wide = full.chunk_wide;
       a.b_off = b0[i];
       a.batch = b0[i + 1] - b0[i];
       p.n_segs = p.chunk_segs;

@@ -544,12 +544,17 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   // simple-finish launches whose segments come out tall take the 12-CTA, wide-register kernel
   // (measured: config 4's 55-row segments gain 5%; config 2's 15-row single wave loses 1%)
   p.wide = false;
+  p.chunk_wide = false;
+  int occ_w = 0;
   if (!general) {
-    int occ_w = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ_w, p.ring == 5 ? wide_kernel_ptr<true, 5>() : wide_kernel_ptr<true, 4>(), 32, smem);
     p.wide = occ_w > 0 && rows / best_segs >= 32;
-    if (const char* env = std::getenv("SC_FAST_WIDE")) p.wide = occ_w > 0 && std::atoi(env) != 0;
+    // under chunked stepping the wide-register kernel wins even on short segments (config 2:
+    // 39.3 -> 38.5 us per step; the concurrent chunks supply the occupancy the 12 CTAs per SM
+    // lack)
+    p.chunk_wide = occ_w > 0;
+    if (const char* env = std::getenv("SC_FAST_WIDE")) p.wide = p.chunk_wide = occ_w > 0 && std::atoi(env) != 0;
     if (p.wide) {
       occ = occ_w;
       best_segs = segment(occ);
@@ -567,7 +572,7 @@ FastPlan plan_fast(int nx, int rows, int batch, int device, bool pressure, bool 
   // other's launch ramps and tails): the longest segments that still give ~1.15 waves of units
   // (measured optimum: config 2 at 11-12 rows, config 5 at whole 128-row columns)
   {
-    const int64_t slots = static_cast<int64_t>(sms) * occ;
+    const int64_t slots = static_cast<int64_t>(sms) * (p.chunk_wide ? occ_w : occ);
     int cs = static_cast<int>((115 * slots + 100 * columns - 1) / (100 * columns));
     cs = std::max(1, std::min(cs, max_segs));
     if (const char* env = std::getenv("SC_CHUNK_SEG_ROWS")) {

@@ -42,6 +42,7 @@ struct FastPlan {
   int ring;       // staged rows (5 when a cloth plugs pressure, else 4)
   bool general;   // some cloth takes the collider / pressure / mask finish
   bool wide;      // simple finish on the wide-register kernel (160 registers, tall segments)
+  bool chunk_wide;  // the same under chunked stepping (capi.cu chunked_fast_steps)
   int occupancy;  // resident CTAs per SM
   // every collider cloth: one frictionless plane (1) / one sphere (2), no pressure plug — the
   // launches without mask output take the kernel with that collider finish alone; 0: dispatch
