@@ -173,6 +173,7 @@ struct sc_ctx {
   static constexpr int kPipe = 16;
   cudaStream_t pipe_stream[kPipe] = {};
   cudaEvent_t pipe_ev[kPipe + 1] = {};
+  std::vector<cudaEvent_t> band_ev;  // band uploads / downloads of rollout_band_pipelined
 
   size_t elem() const { return prec == SC_F32 ? 4 : 8; }
   int64_t nodes_global() const { return static_cast<int64_t>(nx) * ny; }
@@ -496,6 +497,19 @@ NetConst<double>& net_of<double>(sc_ctx* c) {
   return c->net64;
 }
 
+// Plan of a row-range FAST launch (strip steps, bands): cached per (rows, finish kind); the
+// single-kind collider instantiation carries over from the context plan.
+FastPlan range_plan(sc_ctx* c, int rows, bool gen) {
+  const long long key = (static_cast<long long>(rows) << 1) | (gen ? 1 : 0);
+  auto it = c->plan_cache.find(key);
+  if (it == c->plan_cache.end()) {
+    FastPlan p = plan_fast(c->nx, rows, c->batch, c->device, c->any_pressure, gen);
+    p.only = c->plan.only;
+    it = c->plan_cache.emplace(key, p).first;
+  }
+  return it->second;
+}
+
 // One launch of the fused step (or one operator) on the ctx stream.
 template <typename T>
 void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, double t_next,
@@ -514,15 +528,7 @@ void launch_one(sc_ctx* c, int kind, sc_mode mode, int k, bool t_override, doubl
   if constexpr (std::is_same<T, float>::value) {
     if (kind == KIND_STEP && mode == SC_MODE_FAST && c->fast_ok && c->tmap_ok) {
       FastPlan plan = mask ? c->plan_gen : c->plan;
-      if (u0 != c->u0 || u1 != c->u1) {
-        const bool gen = c->any_general || mask != nullptr;
-        const long long key = (static_cast<long long>(u1 - u0) << 1) | (gen ? 1 : 0);
-        auto it = c->plan_cache.find(key);
-        if (it == c->plan_cache.end())
-          it = c->plan_cache.emplace(key, plan_fast(c->nx, u1 - u0, c->batch, c->device,
-                                                    c->any_pressure, gen)).first;
-        plan = it->second;
-      }
+      if (u0 != c->u0 || u1 != c->u1) plan = range_plan(c, u1 - u0, c->any_general || mask);
       e = launch_fast(a, c->fast, c->tmap[c->cur], plan, stream);
     } else {
       e = launch_parity<float>(a, kind, stream);
@@ -1103,6 +1109,195 @@ bool rollout_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int
   return true;
 }
 
+// Row bands of the diagonal-wavefront rollout below: band i holds rows [tops[i-1], tops[i]).
+// ~12M nodes per band (SC_BAND_ROWS overrides the row count; config 4: 1536 rows, e2e 0.93x
+// the device-resident rate against 0.91x at 1024 and 2048 rows), a quarter and a half band first
+// and last (the first upload and the last download are the exposed transfers); empty when the
+// cloth is too short for a pipeline (< 3 full bands).
+std::vector<int> band_tops(int nx, int ny) {
+  int H = std::max(64, (12 << 20) / std::max(1, nx)) / 2 * 2;
+  if (const char* env = std::getenv("SC_BAND_ROWS")) H = std::max(8, std::atoi(env)) / 2 * 2;
+  const int r0 = std::max(4, H / 4 / 2 * 2), r1 = std::max(4, H / 2 / 2 * 2);
+  const int middle = ny - 2 * (r0 + r1);
+  if (middle < H) return {};
+  const int m = std::max(1, (middle + H / 2) / H);
+  std::vector<int> sizes{r0, r1};
+  for (int j = 0; j < m; ++j)
+    sizes.push_back(static_cast<int>((static_cast<int64_t>(j + 1) * middle) / m -
+                                     (static_cast<int64_t>(j) * middle) / m));
+  sizes.push_back(r1);
+  sizes.push_back(r0);
+  std::vector<int> tops;
+  int t = 0;
+  for (int s : sizes) tops.push_back(t += s);
+  return tops;
+}
+
+// Host -> host FAST rollout of ONE large cloth with the transfers overlapped (config 4: 8192^2,
+// 1.6 GB each way over PCIe against ~120 ms of stepping). Cloth chunks cannot hide anything here
+// — the first timestep needs every row — but the cell reaches only 2 rows per timestep
+// (grid.cpp:24-27; the reference's per-step loop eval.cpp:62-65), so the rollout runs as a
+// diagonal wavefront over row bands. Once the rows below tops[i] are resident (band i uploaded),
+// timestep level L (1..steps) can be advanced on every row below tops[i] - 2L. Iteration i
+// launches, for L = 1..steps in order, the level-L rows that became computable, [T(i-1, L),
+// T(i, L)), while the copy engine uploads band i + 1; the rows that reached the last level are
+// converted back and downloaded on the other PCIe direction while later iterations step, so
+// only the first band's upload and the last rows' download stay exposed. Ping-pong buffers stay
+// valid: level L lives in buffer (cur + L) & 1 and, the levels forming a staircase 2 rows apart,
+// a level-L row is overwritten by level L + 2 only after every level-(L + 1) row that reads it
+// is done. Row-range launches take the same kernels and arithmetic as whole-cloth launches:
+// bit-identical results (tests/test_gpu_pipelined_rollout.py).
+bool rollout_band_pipelined(sc_ctx* c, const void* x0, const void* v0, int steps, int k0,
+                            void* xo, void* vo) {
+  if (const char* env = std::getenv("SC_PIPELINE"))
+    if (std::atoi(env) == 0) return false;
+  if (c->prec != SC_F32 || !c->fast_ok || !c->tmap_ok || c->peer_launch || c->strip_row0 >= 0 ||
+      c->batch != 1 || steps < 2 || !xo || !vo)
+    return false;
+  if (small_usable(c) || wave_preferred(c, steps)) return false;
+  if (!pinned(x0) || !pinned(v0) || !pinned(xo) || !pinned(vo)) return false;
+  const std::vector<int> tops = band_tops(c->nx, c->ny);
+  const int nb = static_cast<int>(tops.size());
+  if (nb < 3) return false;
+  // iteration i runs on compute stream q[i & 1]; its launch of level L waits for iteration i-1's
+  // level L-1 (the rows below its band at the level it reads; the only cross-iteration
+  // dependency: iteration i-1 never waits on i, and the staircase keeps their reads and writes on
+  // disjoint rows), so two iterations step concurrently and one launch's tail overlaps the other's
+  // ramp. Iteration i-1 records an event after its layout conversion (level 0) and after every
+  // G-th level; a wait takes the first recorded level >= the one needed.
+  int G = 4;
+  if (const char* env = std::getenv("SC_BAND_G")) G = std::max(1, std::atoi(env));
+  bool chunk_plan = true;
+  if (const char* env = std::getenv("SC_BAND_PLAN")) chunk_plan = std::atoi(env) != 0;
+  const int nlev = steps / G + 2;  // recorded levels per iteration: 0, G, 2G, ..., last
+  for (int i = 0; i < 4; ++i)
+    if (!c->pipe_stream[i])
+      ck(cudaStreamCreateWithFlags(&c->pipe_stream[i], cudaStreamNonBlocking), "stream");
+  if (!c->pipe_ev[16]) ck(cudaEventCreateWithFlags(&c->pipe_ev[16], cudaEventDisableTiming), "event");
+  const int n_ev = 2 * nb + 2 * nlev + 2;  // band uploads, downloads, level events of 2 iterations
+  while (static_cast<int>(c->band_ev.size()) < n_ev) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    c->band_ev.push_back(e);
+  }
+  const int nx = c->nx, ny = c->ny;
+  const size_t row_bytes = static_cast<size_t>(nx) * 3 * sizeof(float);
+  const size_t bytes = row_bytes * ny;
+  c->aos.ensure(2 * bytes);
+  unsigned char* dx = c->aos.p;
+  unsigned char* dv = c->aos.p + bytes;
+  const int64_t S = c->plane_stride;
+  const int cur0 = c->cur;
+  float* st[2] = {static_cast<float*>(c->state[cur0]), static_cast<float*>(c->state[cur0 ^ 1])};
+  cudaStream_t in = c->pipe_stream[0], out = c->pipe_stream[1];
+  cudaStream_t q[2] = {c->pipe_stream[2], c->pipe_stream[3]};
+  auto top = [&](int i, int L) {  // rows below which level L is done after iteration i
+    if (i < 0) return 0;
+    if (tops[i] >= ny) return ny;
+    return std::max(0, tops[i] - 2 * L);
+  };
+  ck(cudaEventRecord(c->pipe_ev[16], c->stream), "event");  // earlier work on the ctx stream
+  for (cudaStream_t w : {in, q[0], q[1]}) ck(cudaStreamWaitEvent(w, c->pipe_ev[16], 0), "wait");
+  for (int i = 0; i < nb; ++i) {
+    const int r0 = i ? tops[i - 1] : 0;
+    const size_t off = row_bytes * r0, n = row_bytes * (tops[i] - r0);
+    ck(cudaMemcpyAsync(dx + off, static_cast<const unsigned char*>(x0) + off, n,
+                       cudaMemcpyHostToDevice, in), "H2D x");
+    ck(cudaMemcpyAsync(dv + off, static_cast<const unsigned char*>(v0) + off, n,
+                       cudaMemcpyHostToDevice, in), "H2D v");
+    ck(cudaEventRecord(c->band_ev[i], in), "event");
+  }
+  StepArgs<float> a = base_args<float>(c);
+  a.net = c->net32;
+  a.health = c->health_on ? c->health.p : nullptr;
+  int64_t launches = 0;
+  // recorded levels of the previous iteration (ascending) and their events
+  std::vector<int> prev_lv, cur_lv;
+  std::vector<cudaEvent_t> prev_ev, cur_ev;
+  for (int i = 0; i < nb; ++i) {
+    const int r0 = i ? tops[i - 1] : 0;
+    cudaStream_t w = q[i & 1];
+    cudaEvent_t* lev = c->band_ev.data() + 2 * nb + (i & 1) * nlev;
+    cur_lv.clear();
+    cur_ev.clear();
+    size_t pk = 0;  // next candidate in prev_lv
+    auto wait_prev = [&](int need) {  // iteration i-1 done with level `need`
+      if (prev_lv.empty()) return;
+      while (pk + 1 < prev_lv.size() && prev_lv[pk] < need) ++pk;
+      ck(cudaStreamWaitEvent(w, prev_ev[pk], 0), "wait");
+    };
+    ck(cudaStreamWaitEvent(w, c->band_ev[i], 0), "wait");
+    ck(launch_aos_to_planar_rows(reinterpret_cast<const float*>(dx + row_bytes * r0),
+                                 reinterpret_cast<const float*>(dv + row_bytes * r0), st[0], nx,
+                                 r0, tops[i] - r0, S, c->pitch, c->zs, w),
+       "aos_to_planar");
+    ck(cudaEventRecord(lev[0], w), "event");
+    cur_lv.push_back(0);
+    cur_ev.push_back(lev[0]);
+    int last = 0;
+    for (int L = 1; L <= steps; ++L) {
+      const int lo = top(i - 1, L), hi = top(i, L);
+      if (hi <= lo) continue;
+      wait_prev(L - 1);
+      a.in = st[(L - 1) & 1];
+      a.out = st[L & 1];
+      a.k = k0 + L - 1;
+      a.u0 = lo;
+      a.u1 = hi;
+      FastPlan pl = range_plan(c, hi - lo, c->any_general);
+      if (chunk_plan) {  // the chunked-stepping segmentation: concurrent launches fill the slots
+        pl.wide = pl.chunk_wide;
+        pl.n_segs = pl.chunk_segs;
+        pl.seg_rows = (hi - lo + pl.n_segs - 1) / pl.n_segs;
+        pl.units = static_cast<int64_t>(a.batch) * pl.n_strips * pl.n_segs;
+      }
+      ck(launch_fast(a, c->fast, c->tmap[cur0 ^ ((L - 1) & 1)], pl, w), "kernel launch");
+      ++launches;
+      last = L;
+      if (L % G == 0) {
+        cudaEvent_t e = lev[cur_ev.size()];
+        ck(cudaEventRecord(e, w), "event");
+        cur_lv.push_back(L);
+        cur_ev.push_back(e);
+      }
+    }
+    if (cur_lv.back() != last) {
+      cudaEvent_t e = lev[cur_ev.size()];
+      ck(cudaEventRecord(e, w), "event");
+      cur_lv.push_back(last);
+      cur_ev.push_back(e);
+    }
+    const int f0 = top(i - 1, steps), f1 = top(i, steps);  // rows at the last level
+    if (f1 > f0) {
+      ck(launch_planar_to_aos_rows(st[steps & 1], reinterpret_cast<float*>(dx + row_bytes * f0),
+                                   reinterpret_cast<float*>(dv + row_bytes * f0), nx, f0,
+                                   f1 - f0, S, c->pitch, c->zs, w),
+         "planar_to_aos");
+      ck(cudaEventRecord(c->band_ev[nb + i], w), "event");
+      ck(cudaStreamWaitEvent(out, c->band_ev[nb + i], 0), "wait");
+      const size_t off = row_bytes * f0, n = row_bytes * (f1 - f0);
+      ck(cudaMemcpyAsync(static_cast<unsigned char*>(xo) + off, dx + off, n,
+                         cudaMemcpyDeviceToHost, out), "D2H x");
+      ck(cudaMemcpyAsync(static_cast<unsigned char*>(vo) + off, dv + off, n,
+                         cudaMemcpyDeviceToHost, out), "D2H v");
+      launches += 1;
+    }
+    std::swap(prev_lv, cur_lv);
+    std::swap(prev_ev, cur_ev);
+  }
+  // the ctx stream continues after the downloads and both compute streams
+  ck(cudaEventRecord(c->pipe_ev[16], out), "event");
+  ck(cudaStreamWaitEvent(c->stream, c->pipe_ev[16], 0), "wait");
+  for (int j = 0; j < 2; ++j) {
+    cudaEvent_t e = c->band_ev[2 * nb + 2 * nlev + j];
+    ck(cudaEventRecord(e, q[j]), "event");
+    ck(cudaStreamWaitEvent(c->stream, e, 0), "wait");
+  }
+  c->launches.fetch_add(launches + nb);
+  c->cur = cur0 ^ (steps & 1);
+  return true;
+}
+
 }  // namespace
 
 // ============================================================================ C ABI =====
@@ -1158,6 +1353,7 @@ void sc_ctx_destroy(sc_ctx* c) {
     if (q) cudaStreamDestroy(q);
   for (cudaEvent_t e : c->pipe_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->band_ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1384,7 +1580,8 @@ sc_status sc_rollout(sc_ctx* c, const void* x0, const void* v0, int32_t steps, i
     reset_health(c);
     if (!constrained && mode == SC_MODE_FAST && steps > 0 &&
         (rollout_wave_pipelined(c, x0, v0, steps, k0, x_out, v_out) ||
-         rollout_pipelined(c, x0, v0, steps, k0, x_out, v_out))) {
+         rollout_pipelined(c, x0, v0, steps, k0, x_out, v_out) ||
+         rollout_band_pipelined(c, x0, v0, steps, k0, x_out, v_out))) {
       ck(cudaStreamSynchronize(c->stream), "sync");
       return;
     }

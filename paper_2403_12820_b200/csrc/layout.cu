@@ -9,15 +9,15 @@ namespace {
 template <typename T>
 __global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, T* __restrict__ out,
                               int batch, int nx, int rows, int64_t plane_stride, int pitch,
-                              bool zs) {
+                              bool zs, int row0) {
   const int64_t per = static_cast<int64_t>(rows) * nx;
   const int64_t total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t b = i / per;
     const int64_t node = i - b * per;
-    const int64_t r = node / nx;
-    const int64_t c = node - r * nx;
+    const int64_t r = node / nx + row0;
+    const int64_t c = node - (r - row0) * nx;
     T* o = out + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -30,15 +30,15 @@ __global__ void aos_to_planar(const T* __restrict__ x, const T* __restrict__ v, 
 template <typename T>
 __global__ void planar_to_aos(const T* __restrict__ in, T* __restrict__ x, T* __restrict__ v,
                               int batch, int nx, int rows, int64_t plane_stride, int pitch,
-                              bool zs) {
+                              bool zs, int row0) {
   const int64_t per = static_cast<int64_t>(rows) * nx;
   const int64_t total = per * batch;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t b = i / per;
     const int64_t node = i - b * per;
-    const int64_t r = node / nx;
-    const int64_t c = node - r * nx;
+    const int64_t r = node / nx + row0;
+    const int64_t c = node - (r - row0) * nx;
     const T* s = in + b * 6 * plane_stride;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -61,7 +61,7 @@ cudaError_t launch_aos_to_planar(const T* x, const T* v, T* planar, int batch, i
                                  int64_t plane_stride, int pitch, bool zs, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(batch) * rows * nx;
   aos_to_planar<T><<<grid_for(total), 256, 0, stream>>>(x, v, planar, batch, nx, rows,
-                                                       plane_stride, pitch, zs);
+                                                       plane_stride, pitch, zs, 0);
   return cudaGetLastError();
 }
 
@@ -70,7 +70,27 @@ cudaError_t launch_planar_to_aos(const T* planar, T* x, T* v, int batch, int nx,
                                  int64_t plane_stride, int pitch, bool zs, cudaStream_t stream) {
   const int64_t total = static_cast<int64_t>(batch) * rows * nx;
   planar_to_aos<T><<<grid_for(total), 256, 0, stream>>>(planar, x, v, batch, nx, rows,
-                                                       plane_stride, pitch, zs);
+                                                       plane_stride, pitch, zs, 0);
+  return cudaGetLastError();
+}
+
+// One band of rows [row0, row0 + rows) of a single cloth: x, v point at the band's first AoS
+// node (the pipelined single-cloth rollout, capi.cu rollout_band_pipelined).
+cudaError_t launch_aos_to_planar_rows(const float* x, const float* v, float* planar, int nx,
+                                      int row0, int rows, int64_t plane_stride, int pitch, bool zs,
+                                      cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(rows) * nx;
+  aos_to_planar<float><<<grid_for(total), 256, 0, stream>>>(x, v, planar, 1, nx, rows,
+                                                           plane_stride, pitch, zs, row0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_planar_to_aos_rows(const float* planar, float* x, float* v, int nx, int row0,
+                                      int rows, int64_t plane_stride, int pitch, bool zs,
+                                      cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(rows) * nx;
+  planar_to_aos<float><<<grid_for(total), 256, 0, stream>>>(planar, x, v, 1, nx, rows,
+                                                           plane_stride, pitch, zs, row0);
   return cudaGetLastError();
 }
 

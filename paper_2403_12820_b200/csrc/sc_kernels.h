@@ -104,5 +104,12 @@ cudaError_t launch_aos_to_planar(const T* x_aos, const T* v_aos, T* planar, int 
 template <typename T>
 cudaError_t launch_planar_to_aos(const T* planar, T* x_aos, T* v_aos, int batch, int nx, int rows,
                                  int64_t plane_stride, int pitch, bool zs, cudaStream_t stream);
+// one band of rows [row0, row0 + rows) of a single f32 cloth; x, v point at the band's first node
+cudaError_t launch_aos_to_planar_rows(const float* x, const float* v, float* planar, int nx,
+                                      int row0, int rows, int64_t plane_stride, int pitch, bool zs,
+                                      cudaStream_t stream);
+cudaError_t launch_planar_to_aos_rows(const float* planar, float* x, float* v, int nx, int row0,
+                                      int rows, int64_t plane_stride, int pitch, bool zs,
+                                      cudaStream_t stream);
 
 }  // namespace scb

@@ -113,3 +113,31 @@ def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch
         assert lp == K * (3 + steps)
     else:  # layout in + wavefront + layout out per chunk
         assert lp == 3 * K
+
+
+@pytest.mark.parametrize("cfg_id,n,band,steps", [(4, 512, "64", 37), (4, 384, "32", 150),
+                                                 (3, 512, "48", 40), (4, 256, "16", 2)])
+def test_band_pipelined_rollout_bit_identical(monkeypatch, cfg_id, n, band, steps):
+    """The single-cloth host -> host rollout as a diagonal wavefront over row bands (capi.cu
+    rollout_band_pipelined: band i+1 uploads while the levels computable from bands <= i step,
+    finished rows download behind later bands) against the plain path: bit-identical. Small
+    bands (SC_BAND_ROWS) put many bands on a test-sized grid; 2 * steps > the band height and
+    steps > ny / 2 exercise the staircase's empty and clipped launches."""
+    from paper_2403_12820_b200 import ClothBatch, configs
+    from paper_2403_12820_b200.api import pinned_empty
+    cfg, scenes, p, x, v = configs.build(cfg_id, batch=1, n=n)
+    xp, vp = pinned_empty(x.shape), pinned_empty(v.shape)
+    xp[...] = x
+    vp[...] = v
+    monkeypatch.setenv("SC_BAND_ROWS", band)
+    with ClothBatch(scenes, p) as cb:
+        xa, va = cb.rollout(x, v, steps, 3, "fast")  # pageable: plain path
+        l0 = cb.launch_count()
+        xo, vo = pinned_empty(x.shape), pinned_empty(v.shape)
+        xb, vb = cb.rollout(xp, vp, steps, 3, "fast", out=(xo, vo))  # pinned: band pipeline
+        lp = cb.launch_count() - l0
+        monkeypatch.setenv("SC_PIPELINE", "0")
+        xc, vc = cb.rollout(xp, vp, steps, 3, "fast")
+    assert bits_equal(xb, xa) and bits_equal(vb, va)
+    assert bits_equal(xc, xa) and bits_equal(vc, va)
+    assert lp > steps + 2  # several row-range launches per level: the band path ran
