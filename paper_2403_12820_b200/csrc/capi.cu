@@ -729,17 +729,25 @@ int fast_chunks(const sc_ctx* c, int steps) {
   return k;
 }
 
-// The wavefront kernel wins on large narrow-cloth batches; below ~8 cloths per SM its whole
-// cloths per CTA quantise the load (config-5 shares: 512 cloths 82.8 vs 75.1 us per step for
-// the chunked streaming path, 1024: 148.1 vs 145.1; 2048: 290.5 vs 305.8), so smaller batches
-// that can be chunked take the streaming kernel. SC_WAVE_MIN_CLOTHS overrides the threshold.
+// The wavefront kernel wins on large narrow-cloth batches stepped for long; below ~8 cloths per
+// SM its whole cloths per CTA quantise the load (config-5 shares: 512 cloths 82.8 vs 75.1 us per
+// step for the chunked streaming path, 1024: 148.1 vs 145.1; 2048: 290.5 vs 305.8), so smaller
+// batches that can be chunked take the streaming kernel. So do short advances: at full clocks the
+// chunked streaming kernel steps config 5 faster (538 vs 561-594 us per timestep), but it moves
+// 48 B per node-update through HBM and after ~50 ms of back-to-back steps the board hits its
+// power cap (sw_power_cap, SM clock 1965 -> ~1600 MHz: 584 us at 150 steps, 617 at 300), while
+// the wavefront kernel (0.06x the DRAM traffic, ~100 W less) holds 1965 MHz (561 us at 300).
+// Measured crossover between 80 and 150 timesteps per call (tools/k_probe.py).
+// SC_WAVE_MIN_CLOTHS / SC_WAVE_MIN_STEPS override the thresholds.
 bool wave_preferred(const sc_ctx* c, int steps) {
   if (!wave_usable(c)) return false;
+  if (fast_chunks(c, steps) == 0) return true;  // no chunked alternative
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  int min_cloths = 8 * sms;
+  int min_cloths = 8 * sms, min_steps = 128;
   if (const char* env = std::getenv("SC_WAVE_MIN_CLOTHS")) min_cloths = std::atoi(env);
-  return c->batch >= min_cloths || fast_chunks(c, steps) == 0;
+  if (const char* env = std::getenv("SC_WAVE_MIN_STEPS")) min_steps = std::atoi(env);
+  return c->batch >= min_cloths && steps >= min_steps;
 }
 
 template <typename Pre, typename Post>

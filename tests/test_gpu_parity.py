@@ -270,6 +270,7 @@ def test_fast_persistent_kernel_matches_per_step_launches(monkeypatch, cfg_id, n
     from paper_2403_12820_b200 import ClothBatch, configs
     monkeypatch.setenv("SC_SMALL", "0")
     monkeypatch.setenv("SC_WAVE_MIN_CLOTHS", "1")  # the wavefront kernel at these batch sizes
+    monkeypatch.setenv("SC_WAVE_MIN_STEPS", "1")  # ... and step counts
     cfg, scenes, p, x, v = configs.build(cfg_id, batch=batch, n=n)
     with ClothBatch(scenes, p) as cb:
         cb.set_persistent(True)

@@ -94,6 +94,7 @@ def test_wave_pipelined_rollout_bit_identical(monkeypatch, cfg_id, chunks, batch
     xp[...] = x
     vp[...] = v
     monkeypatch.setenv("SC_WAVE_MIN_CLOTHS", "1")  # the wavefront pipeline at these batch sizes
+    monkeypatch.setenv("SC_WAVE_MIN_STEPS", "1")  # ... and step counts
     if chunks != "ramp":
         monkeypatch.setenv("SC_WAVE_CHUNKS", chunks)
     else:

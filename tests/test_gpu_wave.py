@@ -15,6 +15,7 @@ def _wave_at_any_batch(monkeypatch):
     """These tests exercise the wavefront kernel itself: take it whatever the batch size (the
     default prefers chunked streaming below 8 cloths per SM, capi.cu wave_preferred)."""
     monkeypatch.setenv("SC_WAVE_MIN_CLOTHS", "1")
+    monkeypatch.setenv("SC_WAVE_MIN_STEPS", "1")  # ... and whatever the step count
 
 
 def bits_equal(a, b):
