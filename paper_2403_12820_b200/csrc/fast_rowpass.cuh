@@ -647,6 +647,27 @@ __device__ __forceinline__ Colliders load_colliders(const StepArgs<float>& a,
 // compiled as straight-line code. Same operations in the same order either way.
 // COLL_PLANE1F: one frictionless plane and no sphere, finished by finish_plane_f.
 constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2, COLL_PLANE1F = 3;
+
+// Broad phase of the one-sphere finish: true when some node of the warp's row may be within
+// `lim` of the sphere (strict: dist <= lim counts; else dist < lim). A node is provably outside
+// when one coordinate alone is: the reference's distance is sqrt_rn of a round-to-nearest sum of
+// squares, each partial sum >= any of its terms (rounding is monotonic) and sqrt_rn(fl(r^2)) =
+// |r|, so |r_d| > lim implies dist > lim (and |r_d| >= lim implies dist >= lim) — the response
+// (kernels.hpp:213-225 / 229-244) is then a no-op for every node of the row, bit for bit, and the
+// warp skips it (a uniform branch). Non-finite coordinates compare false and take the full path.
+__device__ __forceinline__ bool sphere_near(const SphereConst<float>& sp, float lim, bool strict,
+                                            const float (&px)[4], const float (&py)[4],
+                                            const float (&pz)[4]) {
+  bool far = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float r0 = fabsf(__fsub_rn(px[q], sp.c[0])), r1 = fabsf(__fsub_rn(py[q], sp.c[1])),
+                r2 = fabsf(__fsub_rn(pz[q], sp.c[2]));
+    far = far && (strict ? (r0 > lim || r1 > lim || r2 > lim)
+                         : (r0 >= lim || r1 >= lim || r2 >= lim));
+  }
+  return __ballot_sync(__activemask(), !far) != 0u;
+}
 template <int CS = COLL_ANY>
 __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const ClothConst<float>& cc,
                                                const Colliders& col, int b, int k, int Rf,
@@ -723,7 +744,9 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
     }
   };
   if constexpr (CS == COLL_SPHERE1) {
-    sphere_vel(col.s0);
+    const float ox[4] = {xs[0].x, xs[1].x, xs[2].x, xs[3].x};
+    const float oy[4] = {xs[0].y, xs[1].y, xs[2].y, xs[3].y};
+    if (sphere_near(col.s0, col.s0.Rband, true, ox, oy, xz)) sphere_vel(col.s0);
   } else if constexpr (CS == COLL_PLANE1) {
     plane_vel(col.p0);
   } else {
@@ -773,7 +796,10 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
     }
   };
   if constexpr (CS == COLL_SPHERE1) {
-    sphere_pos(col.s0);
+    const float nx4[4] = {xo[0][0], xo[1][0], xo[2][0], xo[3][0]};
+    const float ny4[4] = {xo[0][1], xo[1][1], xo[2][1], xo[3][1]};
+    const float nz4[4] = {xo[0][2], xo[1][2], xo[2][2], xo[3][2]};
+    if (sphere_near(col.s0, col.s0.R, false, nx4, ny4, nz4)) sphere_pos(col.s0);
   } else if constexpr (CS == COLL_PLANE1) {
     plane_pos(col.p0);
   } else {
