@@ -47,8 +47,9 @@ constexpr int ONLY_PLANE_F = 1, ONLY_SPHERE = 2;
 template <bool ALPHA1, int RING, bool PEER = false, bool GEN = true, bool ZS = false,
           int ONLY = 0>
 __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUtensorMap* tmap_z,
-                                         const StepArgs<float>& a, const FastNet& f, int b,
-                                         int strip, int y0, int y1, float* ring, uint64_t* full,
+                                         const StepArgs<float>& a, const FastNet& f,
+                                         const ClothConst<float>& cc, int b, int strip, int y0,
+                                         int y1, float* ring, uint64_t* full,
                                          float (*scratch)[13], uint32_t& phase) {
   const int lane = threadIdx.x;
   const int x0 = strip * STRIP;
@@ -60,14 +61,7 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   const int r_first = y0 - 2;
   const int r_last = y1 + 1;
 
-  // the cloth's constants: loaded before the prologue's TMA waits so the two latencies overlap
-  const ClothConst<float> cc = a.cloths[b];
-  const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
-  const int shape = GEN && !ONLY ? collider_shape(cc, col) : COLL_ANY;
-  const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
-                      a.constrained == nullptr;
   const int64_t nodes = static_cast<int64_t>(nx) * ny;
-  const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
 
   // ring slot t % RING of row r_first + t is tracked incrementally (no modulo in the loop); the
   // TMA operands are formed outside the lane-0 branch so they stay warp-uniform
@@ -103,6 +97,14 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   issue(0, 0);
   issue(1, 1);
   issue(2, 2);
+  // the cloth's constants (their loads were issued before the grid dependency, fast_step_kernel)
+  // are first consumed here, behind the TMA issue: the collider loads that depend on them and the
+  // first rows' flight overlap instead of queueing one L2 round trip after the other
+  const Colliders col = GEN ? load_colliders(a, cc) : Colliders{};
+  const int shape = GEN && !ONLY ? collider_shape(cc, col) : COLL_ANY;
+  const bool simple = cc.n_spheres == 0 && cc.n_planes == 0 && !cc.plug_pressure &&
+                      a.constrained == nullptr;
+  const float t_next = a.use_t_override ? a.t_override : __fmul_rn(float(a.k + 1), cc.dt);
   wait_slot(0);
   wait_slot(1);
 
@@ -384,6 +386,9 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
   decode_unit(unit, n_strips, n_segs, a.u0, a.u1 - a.u0, b, strip, y0, y1);
   b += a.b_off;
   if (a.ids) b = __ldg(a.ids + b);
+  // the cloth's constants do not depend on the previous step: their loads go out before the
+  // grid dependency (consumed in run_unit behind the first TMA issue)
+  const ClothConst<float> cc = a.cloths[b];
   // programmatic dependent launch: the setup above overlapped the previous step's tail; the
   // state it wrote is read from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -397,8 +402,8 @@ __global__ void __launch_bounds__(32, MINB) fast_step_kernel(const __grid_consta
     times[3 * unit + 2] = (static_cast<unsigned long long>(smid) << 32) | wid;
   }
   if (y0 < y1)
-    run_unit<ALPHA1, RING, PEER, GEN, ZS, ONLY>(&tmap_xy, &tmap_z, a, f, b, strip, y0, y1, ring, full, scratch,
-                                 phase);
+    run_unit<ALPHA1, RING, PEER, GEN, ZS, ONLY>(&tmap_xy, &tmap_z, a, f, cc, b, strip, y0, y1, ring,
+                                                full, scratch, phase);
   if (times && threadIdx.x == 0) times[3 * unit + 1] = gtimer();
   // let the next step's grid launch once every CTA of this one is done with its work (an early
   // trigger would let waiting CTAs occupy SM slots a multi-wave grid still needs)
