@@ -337,7 +337,10 @@ __device__ __forceinline__ void run_unit(const CUtensorMap* tmap_xy, const CUten
   }
 }
 
-__device__ unsigned long long* g_unit_times = nullptr;  // debug: [units][3] start, end, sm/warp
+// debug: [units][3] start, end, sm/warp. In constant memory: the pointer is tested at the top of
+// every unit, and a global-memory variable put an L2 round trip (~0.4 us) in front of the first
+// TMA issue (ncu: 4% of config 3's stall samples on that load and its consumers)
+__constant__ unsigned long long* g_unit_times = nullptr;
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
