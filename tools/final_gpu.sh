@@ -20,8 +20,19 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
 SC_BENCH_NVTX=1 timeout 1500 ncu --replay-mode range --nvtx --nvtx-include bench_timed/ --clock-control none --metrics $M -f -o $O/range_cfg5_s20 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-calls 1 > $O/ncu_range5s.log 2>&1; echo "ncu range5 s20 rc=$?"
 SC_BENCH_NVTX=1 timeout 1500 ncu --replay-mode range --nvtx --nvtx-include bench_timed/ --clock-control none --metrics $M -f -o $O/range_cfg4_s20 python bench.py --config 4 --steps 20 --warmup 5 --no-cpu-baseline --e2e-calls 1 > $O/ncu_range4s.log 2>&1; echo "ncu range4 s20 rc=$?"
 SC_BENCH_NVTX=1 timeout 1800 ncu --replay-mode range --nvtx --nvtx-include bench_timed/ --clock-control none --metrics $M -f -o $O/range_cfg5 python bench.py --steps 300 --warmup 3 --no-cpu-baseline --e2e-calls 1 > $O/ncu_range5.log 2>&1; echo "ncu range5 rc=$?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:fast_step_kernel -s 60 -c 1 -f -o $O/fast_cfg5_s20 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-calls 1 > $O/ncu_full5s.log 2>&1; echo "ncu full5 s20 rc=$?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:wave_kernel -s 1 -c 1 -f -o $O/wave_cfg5 python bench.py --steps 300 --warmup 3 --no-cpu-baseline --e2e-calls 1 > $O/ncu_wave.log 2>&1; echo "ncu wave rc=$?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:fast_step_kernel -s 10 -c 1 -f -o $O/step_cfg3 python bench.py --config 3 --steps 30 --warmup 3 --no-cpu-baseline --e2e-calls 1 > $O/ncu_cfg3.log 2>&1; echo "ncu cfg3 rc=$?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:fast_step_kernel -s 5 -c 1 -f -o $O/step_cfg4 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline --e2e-calls 1 > $O/ncu_cfg4.log 2>&1; echo "ncu cfg4 rc=$?"
-for f in range_cfg5_s20 range_cfg4_s20 range_cfg5; do ncu -i $O/$f.ncu-rep --page raw --csv > $O/$f.csv 2>/dev/null; done
+# full captures: summarised on the box (tools/ncu_summary.py), the reports themselves stay there
+# (gpurun brings back at most 64 MiB) except the wavefront one
+full() {  # name, kernel regex, skip, node-updates per launch, title, bench args...
+  local name=$1 rx=$2 skip=$3 nu=$4 title=$5; shift 5
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$rx -s $skip -c 1 -f -o $O/$name python bench.py "$@" --no-cpu-baseline --e2e-calls 1 > $O/ncu_$name.log 2>&1; echo "ncu $name rc=$?"
+  python tools/ncu_summary.py $O/$name.ncu-rep $nu "$title" $O/$name.txt > /dev/null 2>&1; echo "summary $name rc=$?"
+}
+full fast_cfg5_s20 fast_step_kernel 60 $((1024*128*128)) "r02 (final code, the driver's command form): one timed launch of fast_step_kernel on ONE of the four concurrent cloth chunks of config 5 (1024 cloths, whole-column units), captured alone (-k regex:fast_step_kernel -s 60 -c 1): the timed step runs four such launches at once (range replay: r02_range_bench_cfg5_s20.txt)" --steps 20 --warmup 5
+rm -f $O/fast_cfg5_s20.ncu-rep
+full step_cfg3 fast_step_kernel 10 $((1024*1024)) "r02 (final code): fast_step_kernel<ALPHA1, RING 4, GEN, ONLY_SPHERE, plain z> of bench.py --config 3, one timestep of the 1024^2 cloth (5-row single-warp units); -k regex:fast_step_kernel -s 10 -c 1" --config 3 --steps 30 --warmup 3
+rm -f $O/step_cfg3.ncu-rep
+full step_cfg4 fast_step_kernel 5 $((8192*8192)) "r02 (final code): fast_step_kernel (simple finish, wide-register) of bench.py --config 4, one timestep of the 8192^2 cloth; -k regex:fast_step_kernel -s 5 -c 1" --config 4 --steps 10 --warmup 3
+rm -f $O/step_cfg4.ncu-rep
+full wave_cfg5 wave_kernel 1 $((2731*128*128*300)) "r02 (final code): wave_kernel<ALPHA1, W=12, FIN=0> of bench.py --config 5, the timed launch (2731 collider-free cloths of 128^2 on 100 SMs, 300 timesteps; the plane cloths run concurrently in the streaming kernel, not under this capture); -k regex:wave_kernel -s 1 -c 1" --steps 300 --warmup 3
+for f in range_cfg5_s20 range_cfg4_s20 range_cfg5; do ncu -i $O/$f.ncu-rep --page raw --csv > $O/$f.csv 2>/dev/null; rm -f $O/$f.ncu-rep; done
+du -sh $O

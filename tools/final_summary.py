@@ -83,35 +83,14 @@ def main():
                    "source": "profiles/%s (ncu range replay of the whole timed region of "
                              "bench.py --config %d --steps %d)" % (out, cid, steps)}
     json.dump(tj, open(os.path.join(PRO, "traffic.json"), "w"), indent=1)
-    summ = os.path.join(ROOT, "tools", "ncu_summary.py")
-    for rep, nodes, title, out in [
-        ("fast_cfg5_s20", 1024 * 128 * 128,
-         "r02 (final code, the driver's command form): one timed launch of fast_step_kernel on ONE "
-         "of the four concurrent cloth chunks of config 5 (1024 cloths, whole-column units), "
-         "captured alone (-k regex:fast_step_kernel -s 60 -c 1): the timed step runs four such "
-         "launches at once (range replay: r02_range_bench_cfg5_s20.txt)",
-         "r02_fast_step_chunk_cfg5_s20.txt"),
-        ("step_cfg3", 1024 * 1024,
-         "r02 (final code): fast_step_kernel<ALPHA1, RING 4, GEN, ONLY_SPHERE, plain z> of bench.py "
-         "--config 3, one timestep of the 1024^2 cloth (5-row single-warp units); -k "
-         "regex:fast_step_kernel -s 10 -c 1", "r02_fast_step_cfg3.txt"),
-        ("step_cfg4", 8192 * 8192,
-         "r02 (final code): fast_step_kernel (simple finish, wide-register) of bench.py --config 4, "
-         "one timestep of the 8192^2 cloth; -k regex:fast_step_kernel -s 5 -c 1",
-         "r02_fast_step_cfg4.txt")]:
-        subprocess.run([sys.executable, summ, os.path.join(SRC, rep + ".ncu-rep"), str(nodes), title,
-                        os.path.join(PRO, out)], check=True, stdout=subprocess.DEVNULL)
-    # the timed wavefront launch (the collider-free cloths of config 5)
+    # kernel summaries written on the GPU box by tools/ncu_summary.py (final_gpu.sh)
+    for src, out in [("fast_cfg5_s20.txt", "r02_fast_step_chunk_cfg5_s20.txt"),
+                     ("step_cfg3.txt", "r02_fast_step_cfg3.txt"),
+                     ("step_cfg4.txt", "r02_fast_step_cfg4.txt"),
+                     ("wave_cfg5.txt", "r02_wave_bench_cfg5.txt")]:
+        shutil.copy(os.path.join(SRC, src), os.path.join(PRO, out))
     wn = 2731 * 128 * 128
-    out = subprocess.run([sys.executable, summ, os.path.join(SRC, "wave_cfg5.ncu-rep"),
-                          str(wn * 300),
-                          "r02 (final code): wave_kernel<ALPHA1, W=12, FIN=0> of bench.py --config 5, "
-                          "the timed launch (2731 collider-free cloths of 128^2 on 100 SMs, 300 "
-                          "timesteps; the plane cloths run concurrently in the streaming kernel, not "
-                          "under this capture); -k regex:wave_kernel -s 1 -c 1",
-                          os.path.join(PRO, "r02_wave_bench_cfg5.txt")], check=True,
-                         capture_output=True, text=True).stdout
-    for ln in out.splitlines():
+    for ln in open(os.path.join(SRC, "wave_cfg5.txt")):
         if ln.startswith("dram traffic per launch"):
             tj["wave_kernel:cfg5_4096x128x128"] = {
                 "dram_bytes": float(ln.split(":")[1].split("(")[0]), "nodes": wn, "steps": 300,
