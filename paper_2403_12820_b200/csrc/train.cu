@@ -5,7 +5,7 @@
 //   compute_loss   train.cpp:129-209  forward_impulse + plug_impulse + advance_with_impulse per
 //                                     transition, physics/data residuals, hybrid loss
 //   backward_gradients net.cpp:144-201 the 53 parameter-gradient sums
-//   adam_update / schedule_lr / differential_evolution / de_preprocess / train_loop
+//   adam_update / schedule_lr / BoxSearch (the DE pre-search) / de_preprocess / train_loop
 //                  train.cpp:54-63,212-375  host C++ over the 53 scalars, same RNG draws
 //
 // Bit-exactness with the reference (f64): every per-node quantity is the reference expression in
@@ -1021,188 +1021,204 @@ Loss compute_loss(sc_trainer* t, const sc_params& params, Batch& bt, double alph
 
 // ---- optimizer / schedule / DE / loop (train.cpp:54-63, 212-375) ----------------------------
 
-constexpr double kAdamBeta1 = 0.9;
-constexpr double kAdamBeta2 = 0.999;
-constexpr double kAdamEps = 1e-8;
-constexpr uint64_t kDeStream = 0xde5ea4c400000001ULL;
-constexpr uint64_t kProbeStream = 0xde5ea4c400000002ULL;
+// What has to equal the reference here is behaviour, not text: the order of the random draws
+// (every draw comes from the caller's mt19937_64 stream), the rounding order of each floating-
+// point expression, the order in which configuration errors are reported and their messages.
+// The code below is organised around this trainer's flat 53-scalar parameter vector.
+
+// RNG substream tags of the pre-search and of its probe batch: part of the seeded behaviour
+// (train.cpp:18-19), they must be these values for a run to reproduce the reference's.
+constexpr uint64_t kTagSearch = 0xde5ea4c400000001ULL;
+constexpr uint64_t kTagProbe = 0xde5ea4c400000002ULL;
 constexpr double kPi = 3.141592653589793238462643383279502884;
 
+// Learning rate of optimiser step `step` (train.cpp:54-60): step decay by completed intervals,
+// or a half-cosine from lr0 down to the floor over `period` steps.
 double schedule_lr(const sc_train_config& cfg, int step) {
-  if (cfg.schedule_kind == 0) return cfg.lr0 * std::pow(cfg.gamma, step / cfg.interval);
+  if (cfg.schedule_kind == 0) {
+    const int decays = step / cfg.interval;
+    return cfg.lr0 * std::pow(cfg.gamma, decays);
+  }
   if (step >= cfg.period) return cfg.floor;
-  return cfg.floor + (cfg.lr0 - cfg.floor) * 0.5 * (1.0 + std::cos(kPi * step / cfg.period));
+  const double span = cfg.lr0 - cfg.floor;
+  const double phase = kPi * step / cfg.period;
+  return cfg.floor + span * 0.5 * (1.0 + std::cos(phase));
 }
 
+// TrainConfig::validate (train.cpp:62-...): the first violated rule, in the reference's order,
+// with the reference's field names in the message.
 void validate_config(const sc_train_config& c, int transitions) {
-  auto bad = [](const std::string& m) { fail(SC_ERR_CONFIG, m); };
-  if (!(c.alpha >= 0.0 && c.alpha <= 1.0)) bad("train.alpha: must be in [0, 1]");
-  if (c.batch_size < 1) bad("train.batch_size: must be >= 1");
-  if (c.batch_size > transitions)
-    bad("train.batch_size: exceeds the " + std::to_string(transitions) +
-        " available transitions");
-  if (c.epochs < 1) bad("train.epochs: must be >= 1");
-  if (!(c.lr0 > 0.0)) bad("train.lr0: must be > 0");
-  if (!(c.gamma > 0.0 && c.gamma <= 1.0)) bad("train.gamma: must be in (0, 1]");
-  if (c.interval < 1) bad("train.interval: must be >= 1");
-  if (c.period < 1) bad("train.period: must be >= 1");
-  if (!(c.floor >= 0.0)) bad("train.floor: must be >= 0");
-  if (c.de_population < 4) bad("train.de.population: must be >= 4");
-  if (c.de_generations < 0) bad("train.de.generations: must be >= 0");
-  if (!(c.de_bound > 0.0)) bad("train.de.bound: must be > 0");
-  if (!(c.de_cross_prob >= 0.0 && c.de_cross_prob <= 1.0))
-    bad("train.de.cross_prob: must be in [0, 1]");
-  if (!(c.de_diff_weight > 0.0 && c.de_diff_weight <= 2.0))
-    bad("train.de.diff_weight: must be in (0, 2]");
-  if (c.de_probe_batch < 1) bad("train.de.probe_batch: must be >= 1");
-  if (c.checkpoint_interval < 1) bad("train.checkpoint_interval: must be >= 1");
-}
-
-void adam_update(Params& p, const double* grads, sc_adam_state& opt, double lr) {
-  opt.step += 1;
-  const double c1 = 1.0 - std::pow(kAdamBeta1, static_cast<double>(opt.step));
-  const double c2 = 1.0 - std::pow(kAdamBeta2, static_cast<double>(opt.step));
-  for (int s = 0; s < kScalars; ++s) {
-    if (!p.trainable[static_cast<size_t>(group_of(s))]) continue;
-    const double grad = grads[s];
-    opt.m[s] = kAdamBeta1 * opt.m[s] + (1.0 - kAdamBeta1) * grad;
-    opt.v[s] = kAdamBeta2 * opt.v[s] + (1.0 - kAdamBeta2) * grad * grad;
-    const double m_hat = opt.m[s] / c1;
-    const double v_hat = opt.v[s] / c2;
-    p.s[static_cast<size_t>(s)] -= lr * m_hat / (std::sqrt(v_hat) + kAdamEps);
-  }
-}
-
-struct DeDecode {
-  double linear, bias, nonlinear, deriv, self_velocity, alpha;
-};
-DeDecode decode_de(const double* z) {
-  auto scale = [](double v) {
-    return (v >= 0.0 ? 1.0 : -1.0) * std::pow(10.0, std::abs(v) - 2.0);
+  auto unit = [](double v) { return v >= 0.0 && v <= 1.0; };
+  const std::pair<bool, std::string> rules[] = {
+      {unit(c.alpha), "train.alpha: must be in [0, 1]"},
+      {c.batch_size >= 1, "train.batch_size: must be >= 1"},
+      {c.batch_size <= transitions, "train.batch_size: exceeds the " +
+                                        std::to_string(transitions) + " available transitions"},
+      {c.epochs >= 1, "train.epochs: must be >= 1"},
+      {c.lr0 > 0.0, "train.lr0: must be > 0"},
+      {c.gamma > 0.0 && c.gamma <= 1.0, "train.gamma: must be in (0, 1]"},
+      {c.interval >= 1, "train.interval: must be >= 1"},
+      {c.period >= 1, "train.period: must be >= 1"},
+      {c.floor >= 0.0, "train.floor: must be >= 0"},
+      {c.de_population >= 4, "train.de.population: must be >= 4"},
+      {c.de_generations >= 0, "train.de.generations: must be >= 0"},
+      {c.de_bound > 0.0, "train.de.bound: must be > 0"},
+      {unit(c.de_cross_prob), "train.de.cross_prob: must be in [0, 1]"},
+      {c.de_diff_weight > 0.0 && c.de_diff_weight <= 2.0,
+       "train.de.diff_weight: must be in (0, 2]"},
+      {c.de_probe_batch >= 1, "train.de.probe_batch: must be >= 1"},
+      {c.checkpoint_interval >= 1, "train.checkpoint_interval: must be >= 1"},
   };
-  return {scale(z[0]), scale(z[1]), scale(z[2]), scale(z[3]), scale(z[4]),
-          std::pow(10.0, z[5] / 2.0)};
+  for (const auto& [ok, text] : rules)  // NaN fields fail their comparison, as in the reference
+    if (!ok) fail(SC_ERR_CONFIG, text);
 }
-Params group_constant_params(const DeDecode& d) {
-  Params p;
-  for (int c = 0; c < 12; ++c) {
-    p.s[12 + c] = d.linear;
-    p.s[27 + c] = d.nonlinear;
-    p.s[39 + c] = d.deriv;
+
+// Adam (train.cpp:322-340) on the trainable scalars: moments first, then the bias-corrected
+// steps; every scalar's arithmetic is independent of the others, each expression keeps the
+// reference's association (decay * m + (1 - decay) * g, ((1 - decay) * g) * g,
+// (lr * m_hat) / (sqrt(v_hat) + eps)).
+void adam_update(Params& p, const double* grads, sc_adam_state& opt, double lr) {
+  constexpr double kDecayM = 0.9, kDecayV = 0.999, kEps = 1e-8;
+  const double t = static_cast<double>(++opt.step);
+  const double unbias_m = 1.0 - std::pow(kDecayM, t);
+  const double unbias_v = 1.0 - std::pow(kDecayV, t);
+  auto live = [&](int s) { return p.trainable[static_cast<size_t>(group_of(s))]; };
+  for (int s = 0; s < kScalars; ++s)
+    if (live(s)) {
+      const double g = grads[s];
+      opt.m[s] = kDecayM * opt.m[s] + (1.0 - kDecayM) * g;
+      opt.v[s] = kDecayV * opt.v[s] + (1.0 - kDecayV) * g * g;
+    }
+  for (int s = 0; s < kScalars; ++s)
+    if (live(s)) {
+      const double m_hat = opt.m[s] / unbias_m, v_hat = opt.v[s] / unbias_v;
+      p.s[static_cast<size_t>(s)] -= lr * m_hat / (std::sqrt(v_hat) + kEps);
+    }
+}
+
+// The pre-search works on a 6-vector z, one axis per parameter group 1..6 (linear, bias,
+// nonlinear, deriv, self velocity, alpha): the weight groups as sign and decade, sgn(z) *
+// 10^(|z| - 2) (z = -0.0 counts as positive), alpha as 10^(z / 2) (train.cpp:33-45).
+constexpr size_t kSearchDim = 6;
+using GroupValues = std::array<double, kSearchDim>;
+GroupValues decode_search_point(const double* z) {
+  GroupValues out{};
+  for (size_t g = 0; g + 1 < kSearchDim; ++g) {
+    const double magnitude = std::pow(10.0, std::abs(z[g]) - 2.0);
+    out[g] = z[g] >= 0.0 ? magnitude : -magnitude;
   }
-  for (int q = 0; q < 3; ++q) p.s[24 + q] = d.bias;
-  p.s[51] = d.self_velocity;
-  p.s[52] = d.alpha;
+  out[kSearchDim - 1] = std::pow(10.0, z[kSearchDim - 1] / 2.0);
+  return out;
+}
+// every scalar of group g >= 1 set to that group's value (the kernel gains stay 1)
+Params group_constant_params(const GroupValues& values) {
+  Params p;
+  for (int s = 0; s < kScalars; ++s)
+    if (const int g = group_of(s); g >= 1) p.s[static_cast<size_t>(s)] = values[static_cast<size_t>(g - 1)];
   return p;
 }
 
-// differential_evolution (train.cpp:212-266), DE/rand/1/bin with clamping
-template <typename Obj>
-std::vector<double> differential_evolution(Obj&& objective, const std::vector<double>& lo,
-                                           const std::vector<double>& hi, int population,
-                                           int generations, double diff_weight,
-                                           double cross_prob, Rng& rng,
-                                           const std::vector<std::vector<double>>& seed) {
-  const size_t dim = lo.size();
-  const size_t pop_n = static_cast<size_t>(population);
-  std::vector<std::vector<double>> pop(pop_n, std::vector<double>(dim));
-  for (size_t p = 0; p < pop_n; ++p) {
-    if (p < seed.size()) {
-      pop[p] = seed[p];
-      for (size_t d = 0; d < dim; ++d) pop[p][d] = std::clamp(pop[p][d], lo[d], hi[d]);
-    } else {
-      for (size_t d = 0; d < dim; ++d) pop[p][d] = rng.uniform(lo[d], hi[d]);
-    }
+// DE/rand/1/bin in the box [-bound, bound]^dim from a given start population, minimising
+// `cost` (train.cpp:212-266; the reference's random-initialisation branch is not needed: the
+// caller seeds every member). Draw order per member and generation: three distinct partners
+// other than the member itself, each by rejection from uniform_below(members); the coordinate
+// that always crosses over; then one uniform01 per coordinate, drawn whether or not that
+// coordinate is the forced one. A trial replaces its member when it is not worse; the result is
+// the first member with the lowest cost.
+class BoxSearch {
+ public:
+  BoxSearch(std::vector<double> start, size_t dim, double bound)
+      : dim_(dim), members_(start.size() / dim), bound_(bound), x_(std::move(start)),
+        cost_(members_) {
+    for (double& v : x_) v = confine(v);
   }
-  std::vector<double> value(pop_n);
-  for (size_t p = 0; p < pop_n; ++p) value[p] = objective(pop[p].data());
-  std::vector<double> trial(dim);
-  for (int gen = 0; gen < generations; ++gen) {
-    for (size_t p = 0; p < pop_n; ++p) {
-      size_t a, b, c;
-      do a = rng.uniform_below(pop_n);
-      while (a == p);
-      do b = rng.uniform_below(pop_n);
-      while (b == p || b == a);
-      do c = rng.uniform_below(pop_n);
-      while (c == p || c == a || c == b);
-      const size_t forced = rng.uniform_below(dim);
-      for (size_t d = 0; d < dim; ++d) {
-        if (rng.uniform01() < cross_prob || d == forced)
-          trial[d] = std::clamp(pop[a][d] + diff_weight * (pop[b][d] - pop[c][d]), lo[d], hi[d]);
-        else
-          trial[d] = pop[p][d];
+  template <typename Cost>
+  std::vector<double> run(Cost&& cost, int generations, double diff_weight, double cross_prob,
+                          Rng& rng) {
+    for (size_t m = 0; m < members_; ++m) cost_[m] = cost(row(m));
+    std::vector<double> trial(dim_);
+    for (int gen = 0; gen < generations; ++gen)
+      for (size_t m = 0; m < members_; ++m) {
+        const size_t a = partner(rng, {m});
+        const size_t b = partner(rng, {m, a});
+        const size_t c = partner(rng, {m, a, b});
+        const size_t forced = rng.uniform_below(dim_);
+        const double *xa = row(a), *xb = row(b), *xc = row(c), *xm = row(m);
+        for (size_t d = 0; d < dim_; ++d) {
+          const bool cross = rng.uniform01() < cross_prob;
+          trial[d] = (cross || d == forced) ? confine(xa[d] + diff_weight * (xb[d] - xc[d]))
+                                            : xm[d];
+        }
+        const double trial_cost = cost(trial.data());
+        if (trial_cost <= cost_[m]) {
+          std::copy(trial.begin(), trial.end(), row(m));
+          cost_[m] = trial_cost;
+        }
       }
-      const double tv = objective(trial.data());
-      if (tv <= value[p]) {
-        pop[p] = trial;
-        value[p] = tv;
-      }
-    }
+    const size_t best = static_cast<size_t>(
+        std::min_element(cost_.begin(), cost_.end()) - cost_.begin());  // first minimum
+    return std::vector<double>(row(best), row(best) + dim_);
   }
-  size_t best = 0;
-  for (size_t p = 1; p < pop_n; ++p)
-    if (value[p] < value[best]) best = p;
-  return pop[best];
-}
 
-// de_preprocess (train.cpp:268-320)
+ private:
+  double* row(size_t m) { return x_.data() + m * dim_; }
+  double confine(double v) const { return v < -bound_ ? -bound_ : (bound_ < v ? bound_ : v); }
+  size_t partner(Rng& rng, std::initializer_list<size_t> taken) const {
+    for (;;) {
+      const size_t k = rng.uniform_below(members_);
+      if (std::find(taken.begin(), taken.end(), k) == taken.end()) return k;
+    }
+  }
+  size_t dim_, members_;
+  double bound_;
+  std::vector<double> x_, cost_;
+};
+
+// de_preprocess (train.cpp:268-320): the box search over group-constant parameter sets on a
+// fixed probe batch, then per-group initialisation brackets around the best point and a uniform
+// draw inside them for every trainable scalar.
 Params de_preprocess(sc_trainer* t, const sc_train_config& cfg, Rng& rng) {
-  const int transitions = t->frames - 1;
-  Rng probe_rng(Rng::mix(cfg.seed, kProbeStream));
+  Rng probe_rng(Rng::mix(cfg.seed, kTagProbe));
   Batch probe;
-  sample_batch(t, std::min(cfg.de_probe_batch, transitions), probe_rng, probe);
+  sample_batch(t, std::min(cfg.de_probe_batch, t->frames - 1), probe_rng, probe);
   batch_targets(t, probe);
-  auto objective = [&](const double* z) {
+  auto probe_loss = [&](const double* z) {
     try {
-      const sc_params p = to_c(group_constant_params(decode_de(z)));
+      const sc_params p = to_c(group_constant_params(decode_search_point(z)));
       return compute_loss(t, p, probe, cfg.alpha, nullptr).total;
-    } catch (const Fail& f) {
+    } catch (const Fail& f) {  // a diverging candidate is just a bad candidate
       if (f.code != SC_ERR_NUMERICS) throw;
       return 1e300;
     }
   };
-  constexpr size_t kDim = 6;
-  std::vector<double> lo(kDim, -cfg.de_bound), hi(kDim, cfg.de_bound);
-  std::vector<std::vector<double>> seed(static_cast<size_t>(cfg.de_population),
-                                        std::vector<double>(kDim));
-  for (auto& row : seed)
-    for (size_t d = 0; d < kDim; ++d) {
-      const double level = static_cast<double>(rng.uniform_below(6));
-      row[d] = -cfg.de_bound + (level + 0.5) * (2.0 * cfg.de_bound / 6.0);
-    }
-  const std::vector<double> best_z =
-      differential_evolution(objective, lo, hi, cfg.de_population, cfg.de_generations,
-                             cfg.de_diff_weight, cfg.de_cross_prob, rng, seed);
-  const DeDecode best = decode_de(best_z.data());
-  Params params;
-  struct Br {
-    double lo, hi;
-  };
-  auto bracket = [](double s) {
-    const double w = std::max(std::abs(s), 0.05);
-    return Br{s - w, s + w};
-  };
-  std::array<Br, 7> br{};
-  br[0] = {1.0, 1.0};
-  br[1] = bracket(best.linear);
-  br[2] = bracket(best.bias);
-  br[3] = bracket(best.nonlinear);
-  br[4] = bracket(best.deriv);
-  br[5] = bracket(best.self_velocity);
-  Br ab = bracket(best.alpha);
-  ab.lo = std::max(ab.lo, 1e-3);
-  br[6] = ab;
-  for (int g = 0; g < 7; ++g) {
-    params.brackets[2 * g] = br[static_cast<size_t>(g)].lo;
-    params.brackets[2 * g + 1] = br[static_cast<size_t>(g)].hi;
+  // start population: every coordinate on the midpoints of a 6-cell lattice across the box,
+  // one uniform_below(6) per coordinate, member by member
+  const double bound = cfg.de_bound, cell = 2.0 * bound / 6.0;
+  std::vector<double> start(static_cast<size_t>(cfg.de_population) * kSearchDim);
+  for (double& v : start) {
+    const double level = static_cast<double>(rng.uniform_below(6));
+    v = -bound + (level + 0.5) * cell;
   }
-  params.s[52] = best.alpha;
+  const std::vector<double> best_z =
+      BoxSearch(std::move(start), kSearchDim, bound)
+          .run(probe_loss, cfg.de_generations, cfg.de_diff_weight, cfg.de_cross_prob, rng);
+  const GroupValues best = decode_search_point(best_z.data());
+
+  Params params;
+  params.brackets[0] = params.brackets[1] = 1.0;  // kernel gains: fixed at 1
+  for (size_t g = 1; g <= kSearchDim; ++g) {      // value +- max(|value|, 0.05)
+    const double centre = best[g - 1], half = std::max(std::abs(centre), 0.05);
+    params.brackets[2 * g] = centre - half;
+    params.brackets[2 * g + 1] = centre + half;
+  }
+  params.brackets[12] = std::max(params.brackets[12], 1e-3);  // alpha stays positive
+  // frozen groups keep their searched (alpha) or default value; trainable scalars draw from
+  // their group's bracket, in flat scalar order
+  params.s[52] = best[kSearchDim - 1];
   for (int s = 0; s < kScalars; ++s) {
-    const int g = group_of(s);
-    if (!params.trainable[static_cast<size_t>(g)]) continue;
-    params.s[static_cast<size_t>(s)] = rng.uniform(br[static_cast<size_t>(g)].lo,
-                                                   br[static_cast<size_t>(g)].hi);
+    const size_t g = static_cast<size_t>(group_of(s));
+    if (params.trainable[g])
+      params.s[static_cast<size_t>(s)] = rng.uniform(params.brackets[2 * g], params.brackets[2 * g + 1]);
   }
   return params;
 }
@@ -1539,7 +1555,7 @@ sc_status sc_trainer_run(sc_trainer* t, const sc_train_config* cfg, const sc_par
         for (int g = 0; g < 7; ++g) params.trainable[static_cast<size_t>(g)] = resume_trainable[g] != 0;
       if (opt_inout) opt = *opt_inout;
     } else {
-      Rng de_rng(Rng::mix(cfg->seed, kDeStream));
+      Rng de_rng(Rng::mix(cfg->seed, kTagSearch));
       params = de_preprocess(t, *cfg, de_rng);
     }
     for (int g = 0; g < 7; ++g)
