@@ -44,6 +44,16 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_NODE_UPDATE = 48  # fp32 x, v: 24 B read + 24 B written per node per timestep
 DEFAULT_CONFIG = 5
+# config.workload of both arms (ours and --impl reference print the same string; the reference
+# arm never imports the product package, tests/test_bench_cli.py keeps this table and
+# paper_2403_12820_b200.configs in step)
+WORKLOAD_LABEL = {
+    1: "cfg1: 1 x 32^2, two top corners pinned, gravity, 100 steps, hidden 8 (3x3)",
+    2: "cfg2: 64 x 256^2, top row pinned, gravity + wind, 1000 steps",
+    3: "cfg3: 1 x 1024^2, two corners pinned, sphere R=0.3 under the cloth, 500 steps",
+    4: "cfg4: 1 x 8192^2, top row pinned, gravity, 200 steps",
+    5: "cfg5: 4096 x 128^2, mixed BCs (top row / corners / free onto plane z=-0.5), wind",
+}
 WORKLOAD_KEY = {1: "cfg1_32x32", 2: "cfg2_64x256x256", 3: "cfg3_1024x1024", 4: "cfg4_8192x8192",
                 5: "cfg5_4096x128x128"}
 
@@ -257,8 +267,11 @@ def run_reference(args, world, rank):
         "warmup": args.warmup, "ms_per_step": 1e3 * total_sec / args.steps,
         "higher_is_better": True, "scaling": "strong" if cid in (2, 4, 5) else "replicas",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w.name, "grid": "%dx%d" % (w.n, w.n),
-                   "sampled": desc, "same_config": False,
+        "config": {"workload": WORKLOAD_LABEL[cid], "grid": "%dx%d" % (w.n, w.n),
+                   "sample_per_step": desc,
+                   "sample_of": "a bounded sample of the same workload per step (every cloth and "
+                                "timestep of it costs the same; its full size takes minutes per "
+                                "rollout on the CPU)",
                    "parallelism": "cpu, %d host threads" % cores},
         "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": cores,
                          "kind": "reference", "sample": sample},
@@ -425,7 +438,8 @@ def run_ours(args, world, rank, local):
                        "(pinned buffers; per-step bytes = the state's in / out over %d)" % (T, T),
                "finite": finite}
         cb.close()
-        conf = {"workload": "cfg%d: %s" % (cid, cfg.description), "cloths": cfg.batch,
+        assert WORKLOAD_LABEL[cid] == "cfg%d: %s" % (cid, cfg.description)
+        conf = {"workload": WORKLOAD_LABEL[cid], "cloths": cfg.batch,
                 "cloths_per_gpu": B, "grid": "%dx%d" % (cfg.n, cfg.n), "nodes_per_gpu": nodes_rank,
                 **({"shared_gpu": "test hook: every rank on GPU 0 (not a measurement)"}
                    if SHARE_GPU and world > 1 else {}),
@@ -485,7 +499,7 @@ def run_ours(args, world, rank, local):
                "d2h_bytes_per_step": 2 * xl.nbytes / T,
                "call": "set_state (host) + %d strip steps + get_state (host)" % T}
         sr.close()
-        conf = {"workload": "cfg4: " + cfg.description, "grid": "8192x8192",
+        conf = {"workload": WORKLOAD_LABEL[4], "grid": "8192x8192",
                 "nodes_per_gpu": nodes_rank, "timesteps_per_step": 1, "mode": mode,
                 "l2": "no flush: state 2 x %.0f MB >> 126 MB L2" % (24e-6 * nodes_rank),
                 "parallelism": "%d row strips, 2-row halo per step %s" % (

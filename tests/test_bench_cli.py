@@ -33,3 +33,18 @@ def test_reference_arm_does_not_load_the_product_library():
     line = json.loads(out[-2])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference"
+    # both arms name the workload with the same string
+    sys.path.insert(0, ROOT)
+    import bench
+    assert line["config"]["workload"] == bench.WORKLOAD_LABEL[5]
+    assert line["metric"] == "cloth node-updates/s" and line["unit"] == "node-updates/s"
+    assert line["e2e"]["value"] == line["value"]
+
+
+def test_workload_labels_match_the_product_configs():
+    """bench.WORKLOAD_LABEL (shared by both arms' config.workload) follows configs.CONFIGS."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2403_12820_b200 import configs
+    for cid, cfg in configs.CONFIGS.items():
+        assert bench.WORKLOAD_LABEL[cid] == "cfg%d: %s" % (cid, cfg.description)
