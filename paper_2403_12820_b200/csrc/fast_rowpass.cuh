@@ -636,111 +636,6 @@ __device__ __forceinline__ Colliders load_colliders(const StepArgs<float>& a,
   return c;
 }
 
-// collider sets of the finish (see finish_general below)
-constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2, COLL_PLANE1F = 3;
-
-// Broad phase of the one-sphere finish: true when some node of the warp's row may be within
-// `lim` of the sphere centre. The response (kernels.hpp:213-225 / 229-244) acts only when the
-// reference's dist = sqrt_rn(S), S the round-to-nearest sum of the squared coordinates of
-// r = x - c, is <= R_band (velocity level) or < R (position level). d2 below is the same sum in
-// contracted arithmetic: both carry at most three roundings over positive terms, so they differ
-// by < 4e-7 relative, and sqrt_rn adds 6e-8. d2 > lim^2 (1 + 2e-5) therefore implies dist > lim
-// strictly, the response would be a no-op for every node of the row, bit for bit, and the warp
-// skips it (warp vote, uniform branch). Non-finite coordinates compare false and take the full
-// path; an overflowing d2 means an infinite dist on both sides.
-__device__ __forceinline__ bool sphere_near(const SphereConst<float>& sp, float lim,
-                                            const float (&px)[4], const float (&py)[4],
-                                            const float (&pz)[4]) {
-  const float lim2 = (lim * lim) * 1.00002f;
-  bool far = true;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float r0 = __fsub_rn(px[q], sp.c[0]), r1 = __fsub_rn(py[q], sp.c[1]),
-                r2 = __fsub_rn(pz[q], sp.c[2]);
-    far = far && fmaf(r0, r0, fmaf(r1, r1, r2 * r2)) > lim2;
-  }
-  return __ballot_sync(__activemask(), !far) != 0u;
-}
-
-// The two sphere responses of the one-sphere finish for the lane's 4 nodes, branch-free: the
-// exact distances first, a warp vote on "some node of the row is in contact" (uniform), then
-// every node runs the response's operations — the same IEEE round-to-nearest operations in the
-// same order as sphere_velocity / sphere_position (sc_device.cuh, kernels.hpp:213-244) — and
-// keeps the result only where the reference's conditions hold (selects instead of the nested,
-// divergent contact branches; a node with dist = 0 or a non-finite distance divides into inf /
-// NaN that no condition selects). Same bits as the per-node calls.
-__device__ __forceinline__ void sphere_velocity4(const SphereConst<float>& sp,
-                                                 const float2 (&xs)[4], const float (&xz)[4],
-                                                 float2 (&vxy)[4], float (&vzz)[4],
-                                                 uint8_t (&mk)[4]) {
-  using R = RN<float>;
-  float r[4][3], dist[4];
-  bool near[4], any = false;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    r[q][0] = R::sub(xs[q].x, sp.c[0]);
-    r[q][1] = R::sub(xs[q].y, sp.c[1]);
-    r[q][2] = R::sub(xz[q], sp.c[2]);
-    dist[q] = R::sqrt(R::add(R::add(R::mul(r[q][0], r[q][0]), R::mul(r[q][1], r[q][1])),
-                             R::mul(r[q][2], r[q][2])));
-    near[q] = dist[q] > 0.f && dist[q] <= sp.Rband;
-    any = any || near[q];
-  }
-  if (__ballot_sync(__activemask(), any) == 0u) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float v[3] = {vxy[q].x, vxy[q].y, vzz[q]};
-    const float vn = R::div(R::add(R::add(R::mul(v[0], r[q][0]), R::mul(v[1], r[q][1])),
-                                   R::mul(v[2], r[q][2])),
-                            dist[q]);
-    const bool hit = near[q] && vn < 0.f;
-    float o[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const float nrm = R::div(r[q][d], dist[q]);
-      o[d] = R::mul(R::sub(v[d], R::mul(nrm, vn)), sp.omf);
-    }
-    vxy[q] = hit ? make_float2(o[0], o[1]) : vxy[q];
-    vzz[q] = hit ? o[2] : vzz[q];
-    mk[q] = hit ? 1 : mk[q];
-  }
-}
-__device__ __forceinline__ void sphere_position4(const SphereConst<float>& sp, float (&xo)[4][3],
-                                                 float (&vo)[4][3], uint8_t (&mk)[4]) {
-  using R = RN<float>;
-  float r[4][3], dist[4];
-  bool inside[4], any = false;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-#pragma unroll
-    for (int d = 0; d < 3; ++d) r[q][d] = R::sub(xo[q][d], sp.c[d]);
-    dist[q] = R::sqrt(R::add(R::add(R::mul(r[q][0], r[q][0]), R::mul(r[q][1], r[q][1])),
-                             R::mul(r[q][2], r[q][2])));
-    inside[q] = dist[q] > 0.f && dist[q] < sp.R;
-    any = any || inside[q];
-  }
-  if (__ballot_sync(__activemask(), any) == 0u) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float nrm[3], px[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      nrm[d] = R::div(r[q][d], dist[q]);
-      px[d] = R::add(sp.c[d], R::mul(nrm[d], sp.R));
-    }
-    const float vn = R::add(R::add(R::mul(vo[q][0], nrm[0]), R::mul(vo[q][1], nrm[1])),
-                            R::mul(vo[q][2], nrm[2]));
-    const bool damp = inside[q] && vn < 0.f;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const float dv = R::mul(R::sub(vo[q][d], R::mul(nrm[d], vn)), sp.omf);
-      xo[q][d] = inside[q] ? px[d] : xo[q][d];
-      vo[q][d] = damp ? dv : vo[q][d];
-    }
-    mk[q] = inside[q] ? 1 : mk[q];
-  }
-}
-
 // Colliders and/or the contact mask: the lane's 4 nodes together, each node through the same
 // IEEE round-to-nearest sequence as advance_with_impulse (sc_device.cuh: plug_tail, the
 // velocity-level response on the old positions, x' = x + v' dt, the position-level projection,
@@ -751,6 +646,28 @@ __device__ __forceinline__ void sphere_position4(const SphereConst<float>& sp, f
 // COLL_PLANE1 (one plane, no sphere: config 5) and COLL_SPHERE1 (one sphere, no plane: config 3),
 // compiled as straight-line code. Same operations in the same order either way.
 // COLL_PLANE1F: one frictionless plane and no sphere, finished by finish_plane_f.
+constexpr int COLL_ANY = 0, COLL_PLANE1 = 1, COLL_SPHERE1 = 2, COLL_PLANE1F = 3;
+
+// Broad phase of the one-sphere finish: true when some node of the warp's row may be within
+// `lim` of the sphere (strict: dist <= lim counts; else dist < lim). A node is provably outside
+// when one coordinate alone is: the reference's distance is sqrt_rn of a round-to-nearest sum of
+// squares, each partial sum >= any of its terms (rounding is monotonic) and sqrt_rn(fl(r^2)) =
+// |r|, so |r_d| > lim implies dist > lim (and |r_d| >= lim implies dist >= lim) — the response
+// (kernels.hpp:213-225 / 229-244) is then a no-op for every node of the row, bit for bit, and the
+// warp skips it (a uniform branch). Non-finite coordinates compare false and take the full path.
+__device__ __forceinline__ bool sphere_near(const SphereConst<float>& sp, float lim, bool strict,
+                                            const float (&px)[4], const float (&py)[4],
+                                            const float (&pz)[4]) {
+  bool far = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float r0 = fabsf(__fsub_rn(px[q], sp.c[0])), r1 = fabsf(__fsub_rn(py[q], sp.c[1])),
+                r2 = fabsf(__fsub_rn(pz[q], sp.c[2]));
+    far = far && (strict ? (r0 > lim || r1 > lim || r2 > lim)
+                         : (r0 >= lim || r1 >= lim || r2 >= lim));
+  }
+  return __ballot_sync(__activemask(), !far) != 0u;
+}
 template <int CS = COLL_ANY>
 __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const ClothConst<float>& cc,
                                                const Colliders& col, int b, int k, int Rf,
@@ -829,8 +746,7 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
   if constexpr (CS == COLL_SPHERE1) {
     const float ox[4] = {xs[0].x, xs[1].x, xs[2].x, xs[3].x};
     const float oy[4] = {xs[0].y, xs[1].y, xs[2].y, xs[3].y};
-    if (sphere_near(col.s0, col.s0.Rband, ox, oy, xz))
-      sphere_velocity4(col.s0, xs, xz, vxy, vzz, mk);
+    if (sphere_near(col.s0, col.s0.Rband, true, ox, oy, xz)) sphere_vel(col.s0);
   } else if constexpr (CS == COLL_PLANE1) {
     plane_vel(col.p0);
   } else {
@@ -883,7 +799,7 @@ __device__ __forceinline__ void finish_general(const StepArgs<float>& a, const C
     const float nx4[4] = {xo[0][0], xo[1][0], xo[2][0], xo[3][0]};
     const float ny4[4] = {xo[0][1], xo[1][1], xo[2][1], xo[3][1]};
     const float nz4[4] = {xo[0][2], xo[1][2], xo[2][2], xo[3][2]};
-    if (sphere_near(col.s0, col.s0.R, nx4, ny4, nz4)) sphere_position4(col.s0, xo, vo, mk);
+    if (sphere_near(col.s0, col.s0.R, false, nx4, ny4, nz4)) sphere_pos(col.s0);
   } else if constexpr (CS == COLL_PLANE1) {
     plane_pos(col.p0);
   } else {
