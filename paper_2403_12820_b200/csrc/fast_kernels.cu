@@ -431,6 +431,9 @@ FastNet make_fast_net(const NetConst<float>& n) {
   f.alpha1 = 1;
   for (int c = 0; c < kChannels; ++c)
     if (f.alpha[c] != 1.0f) f.alpha1 = 0;
+  f.live = 0;
+  for (int c = 0; c < kChannels; ++c)
+    if (f.wl[c] != 0.0f || f.wn[c] != 0.0f || f.wd[c] != 0.0f) f.live |= 1u << c;
   return f;
 }
 

@@ -33,6 +33,11 @@ struct FastNet {
   float b[3];
   float wv;
   int alpha1;  // every alpha' == 1 (default gains and alpha): skips one multiply per edge
+  // channels with a nonzero weight (bit c). A channel whose three weights are all zero
+  // contributes dx * 0 to the cell: the small-cloth kernel skips it (config 1's
+  // "hidden 8, 3x3" cell is the reference cell with the four skip channels zeroed; a non-finite
+  // neighbour then no longer spreads through such a channel, which only PARITY mode reproduces)
+  unsigned live;
 };
 struct FastPlan {
   int n_strips, seg_rows, n_segs;

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kSmallMaxNodes, 1)
     nbr[c] = jy * nx + jx;
     if (jx >= 0 && jx < nx && jy >= 0 && jy < ny) valid |= 1u << c;
   }
+  valid &= f.live;  // zero-weight channels (config 1's skip channels) contribute dx * 0: skipped
   const int64_t gnode = static_cast<int64_t>(iy) * nx + ix;
   __syncthreads();
 
